@@ -1,0 +1,432 @@
+#!/usr/bin/env python3
+"""bench.py — L4 hot path on B200: decode-attention KV GB/s (% of HBM peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4] [--impl l4|reference]
+
+A step is one pass of the hot path over one synthetic batch: the length-binned
+work-list build (a1, l4_decode_plan) plus the split-KV kernel with its fused
+LSE combine (a2+a3, l4_decode_run), i.e. one decode iteration of one layer.
+`value` = algorithmic KV bytes per step / device time (GB/s), inputs resident
+in HBM; `e2e` = the same metric through the public API with host buffers
+(q, kv_len and the page table copied H2D, the output D2H, every step).
+The KV working set (1-11 GB) exceeds the 126 MB L2, so no flush is needed.
+
+N > 1 (torchrun): every rank runs its own instance (replicas of the same
+workload, no data-path collective, "weak" scaling); time = max over ranks.
+
+--impl reference: the FP64 CPU oracle (oracle/attention.py), as it stands, on
+a bounded sample of the same workload — the reference arm for this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+WORKLOADS = {
+    "c2": dict(desc="BASELINE configs[1]: Llama-3-8B attention (32q/8kv, d128), bf16, batch 250, uniform 1K contexts",
+               shape=synth.SHAPE_LLAMA3_8B, lens=lambda: synth.lengths_c2()),
+    "c3": dict(desc="BASELINE configs[2]: Llama-3-8B shape, batch 256, ShareGPT-like skewed 100..128K (seed 0), mixed batch",
+               shape=synth.SHAPE_LLAMA3_8B, lens=lambda: synth.lengths_c3(0)),
+    "c4": dict(desc="BASELINE configs[3]: Llama-3-70B attention (64q/8kv), long-context batch 32, 32K..128K (seed 0)",
+               shape=synth.SHAPE_LLAMA3_70B, lens=lambda: synth.lengths_c4(0)),
+}
+METRIC = "decode-attn KV GB/s (% HBM peak), mixed vs binned; tokens/s at 1/2/4/8 GPUs"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def kv_bytes(lens, shape) -> int:
+    return int(4 * shape.num_kv_heads * shape.head_dim * int(np.sum(lens)))
+
+
+def algo_bytes(lens, shape) -> int:
+    """K+V once + q (bf16) + out (fp32) + page indices."""
+    B = len(lens)
+    pages = sum(synth.pages_for(x) for x in lens)
+    return kv_bytes(lens, shape) + B * shape.num_q_heads * 128 * (2 + 4) + 4 * pages
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, flag in zip(names, parts[5:9]):
+                if flag.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workload
+class Workload:
+    def __init__(self, name: str, lens, shape, seed: int = 0, device="cuda"):
+        import torch
+        self.name, self.shape = name, shape
+        self.lens = np.asarray(lens, dtype=np.int64)
+        self.table = synth.make_page_table(self.lens, seed=seed, spare_pages=64)
+        g = torch.Generator(device=device).manual_seed(seed)
+        B, t = len(self.lens), self.table
+        self.q = torch.randn(B, shape.num_q_heads, 128, device=device, generator=g).to(torch.bfloat16)
+        self.k = torch.empty(t.num_pages, shape.num_kv_heads, 16, 128, dtype=torch.bfloat16, device=device)
+        self.v = torch.empty_like(self.k)
+        for x in (self.k, self.v):      # chunked to bound the fp32 temporary
+            for s in range(0, t.num_pages, 8192):
+                e = min(t.num_pages, s + 8192)
+                x[s:e] = torch.randn(e - s, *x.shape[1:], device=device, generator=g).to(torch.bfloat16)
+        self.indptr = torch.from_numpy(t.indptr).to(device)
+        self.indices = torch.from_numpy(t.indices).to(device)
+        self.kv_len = torch.from_numpy(t.kv_len).to(device)
+        self.out = torch.empty(B, shape.num_q_heads, 128, dtype=torch.float32, device=device)
+        self.lse = torch.empty(B, shape.num_q_heads, dtype=torch.float32, device=device)
+
+    @property
+    def bytes_kv(self):
+        return kv_bytes(self.lens, self.shape)
+
+    @property
+    def bytes_algo(self):
+        return algo_bytes(self.lens, self.shape)
+
+
+def make_l4(wl: Workload):
+    from paper_2512_19179_b200 import l4
+    params = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads)
+    ws = l4.alloc_workspace(params, wl.table.total_pages)
+    return l4, params, ws
+
+
+def time_steps(wl: Workload, steps: int, warmup: int, run_only=False):
+    """Device time of `steps` hot-path steps (plan + run) on the current stream."""
+    import torch
+    l4, params, ws = make_l4(wl)
+    st = torch.cuda.current_stream()
+
+    def step():
+        if not run_only:
+            l4.decode_plan(params, wl.kv_len, wl.indptr, wl.table.total_pages, ws)
+        l4.decode_run(params, wl.q, wl.k, wl.v, wl.indices, wl.out, wl.lse, ws)
+
+    if run_only:
+        l4.decode_plan(params, wl.kv_len, wl.indptr, wl.table.total_pages, ws)
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    evs[0].record(st)
+    for i in range(steps):
+        step()
+        evs[i + 1].record(st)
+    torch.cuda.synchronize()
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+    total = evs[0].elapsed_time(evs[-1])
+    return total, per, l4.plan_info(ws)
+
+
+def time_e2e(wl: Workload, steps: int, warmup: int):
+    """Same metric through the public API with HOST buffers: every step copies q,
+    kv_len, indptr, indices H2D from pinned memory, runs plan+run, copies out D2H."""
+    import torch
+    l4, params, ws = make_l4(wl)
+    st = torch.cuda.current_stream()
+    h_q = wl.q.cpu().pin_memory()
+    h_kl = wl.kv_len.cpu().pin_memory()
+    h_ip = wl.indptr.cpu().pin_memory()
+    h_ix = wl.indices.cpu().pin_memory()
+    h_out = torch.empty(wl.out.shape, dtype=torch.float32).pin_memory()
+    d_q, d_kl, d_ip, d_ix = (torch.empty_like(wl.q), torch.empty_like(wl.kv_len), torch.empty_like(wl.indptr),
+                             torch.empty_like(wl.indices))
+    h2d = sum(t.numel() * t.element_size() for t in (h_q, h_kl, h_ip, h_ix))
+    d2h = h_out.numel() * h_out.element_size()
+
+    def step():
+        d_q.copy_(h_q, non_blocking=True)
+        d_kl.copy_(h_kl, non_blocking=True)
+        d_ip.copy_(h_ip, non_blocking=True)
+        d_ix.copy_(h_ix, non_blocking=True)
+        l4.decode_plan(params, d_kl, d_ip, wl.table.total_pages, ws)
+        l4.decode_run(params, d_q, wl.k, wl.v, d_ix, wl.out, wl.lse, ws)
+        h_out.copy_(wl.out, non_blocking=True)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    e1.synchronize()
+    return e0.elapsed_time(e1), h2d, d2h
+
+
+def cpu_oracle_sample(wl_name: str, budget_s: float = 15.0):
+    """The FP64 oracle, as it stands, on a bounded sample of the workload's requests."""
+    import torch
+    from oracle import attention as oa
+    spec = WORKLOADS[wl_name]
+    shape = spec["shape"]
+    lens = spec["lens"]()
+    order = list(range(len(lens)))
+    # bounded sample: requests in workload order until ~budget_s of CPU work
+    cores = len(os.sched_getaffinity(0))
+    done_tokens, n_req, oracle_time = 0, 0, 0.0
+    g = torch.Generator().manual_seed(1234)
+    for b in order:
+        L = int(lens[b])
+        table = synth.make_page_table([L], seed=b, spare_pages=0, layout="contiguous")
+        q = torch.randn(1, shape.num_q_heads, 128, generator=g).to(torch.bfloat16)
+        k = torch.randn(table.num_pages, shape.num_kv_heads, 16, 128, generator=g).to(torch.bfloat16)
+        v = torch.randn(table.num_pages, shape.num_kv_heads, 16, 128, generator=g).to(torch.bfloat16)
+        t0 = time.perf_counter()        # input generation is excluded; the oracle call is timed
+        oa.paged_decode_attention(q, k, v, table.indptr, table.indices, table.kv_len, shape.num_kv_heads)
+        oracle_time += time.perf_counter() - t0
+        done_tokens += L
+        n_req += 1
+        if oracle_time >= budget_s:
+            break
+    gbs = kv_bytes([done_tokens], shape) / oracle_time / 1e9
+    try:
+        import threadpoolctl
+        blas = max((x.get("num_threads", 1) for x in threadpoolctl.threadpool_info()), default=1)
+    except Exception:
+        blas = None
+    return dict(value=round(gbs, 4), unit="GB/s", cores=cores, kind="oracle",
+                sample=f"first {n_req} of {len(lens)} requests of {wl_name} ({done_tokens} tokens), FP64 NumPy, "
+                       f"{oracle_time:.1f} s; BLAS threads {blas}", seconds=round(oracle_time, 3),
+                tokens=done_tokens, requests=n_req)
+
+
+# ----------------------------------------------------------------------------- binned vs mixed
+def mixed_vs_binned(steps: int, warmup: int):
+    """C3 (seed 0): one mixed call vs the same requests split into power-of-4 length
+    bins (one call per bin, all on one stream); plus C4 as a long-stage batch."""
+    import torch
+    res = {}
+    shape = synth.SHAPE_LLAMA3_8B
+    lens = synth.lengths_c3(0)
+    wl = Workload("c3", lens, shape)
+    tot, _, info = time_steps(wl, steps, warmup)
+    res["c3_mixed"] = dict(gbs=round(wl.bytes_kv / (tot / steps / 1e3) / 1e9, 1), ms=round(tot / steps, 4),
+                           items=info.num_items, chunk_pages=info.chunk_pages)
+    edges = [0, 1024, 4096, 16384, 65536, 1 << 30]
+    t_sum, b_sum, bins = 0.0, 0, []
+    del wl
+    for lo, hi in zip(edges, edges[1:]):
+        sel = lens[(lens >= lo) & (lens < hi)]
+        if len(sel) == 0:
+            continue
+        w = Workload(f"c3[{lo},{hi})", sel, shape)
+        t, _, _ = time_steps(w, steps, warmup)
+        t_sum += t / steps
+        b_sum += w.bytes_kv
+        bins.append(dict(lo=lo, hi=hi if hi < (1 << 30) else None, batch=int(len(sel)),
+                         gbs=round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1)))
+        del w
+    res["c3_binned_same_requests"] = dict(gbs=round(b_sum / (t_sum / 1e3) / 1e9, 1), ms=round(t_sum, 4), bins=bins)
+    torch.cuda.empty_cache()
+    w = Workload("c4", synth.lengths_c4(0), synth.SHAPE_LLAMA3_70B)
+    t, _, info = time_steps(w, steps, warmup)
+    res["c4"] = dict(gbs=round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1), ms=round(t / steps, 4),
+                     items=info.num_items, chunk_pages=info.chunk_pages)
+    del w
+    torch.cuda.empty_cache()
+    return res
+
+
+# ----------------------------------------------------------------------------- main
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    name = args.workload
+    spec = WORKLOADS[name]
+    budget = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(name, budget_s=budget / 4)
+    vals, samples = [], None
+    for _ in range(args.steps):
+        r = cpu_oracle_sample(name, budget_s=budget)
+        vals.append(r["value"])
+        samples = r
+    v = float(np.mean(vals))
+    line = dict(impl="reference", metric=METRIC, value=round(v, 4), unit="GB/s", n_gpus=args.gpus,
+                steps=args.steps, warmup=args.warmup, ms_per_step=None, higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=name, desc=spec["desc"], model=spec["shape"].name, global_batch=len(spec["lens"]())),
+                cpu_baseline=dict(value=round(v, 4), unit="GB/s", cores=samples["cores"], kind="oracle",
+                                  sample=samples["sample"]),
+                e2e=dict(value=round(v, 4), unit="GB/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="l4", choices=["l4", "reference"])
+    ap.add_argument("--no-extra", action="store_true", help="skip mixed-vs-binned / C4 sub-measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_src = load_peaks()
+    spec = WORKLOADS[args.workload]
+    wl = Workload(args.workload, spec["lens"](), spec["shape"], seed=rank)
+    from paper_2512_19179_b200 import l4
+
+    # warm-up + build plan once for run-only timing
+    time_steps(wl, 2, args.warmup)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    total_ms, per, info = time_steps(wl, args.steps, 0)
+    run_ms, run_per, _ = time_steps(wl, args.steps, 1, run_only=True)
+    clk = clocks.stop()
+    if ws > 1:
+        t = torch.tensor([total_ms, run_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+        total_ms, run_ms = float(t[0]), float(t[1])
+    ms_step = total_ms / args.steps
+    value = ws * wl.bytes_kv / (ms_step / 1e3) / 1e9
+    # roofline of the dominant kernel (decode_kernel): algorithmic bytes / its launch time
+    run_avg = run_ms / args.steps
+    achieved = wl.bytes_algo / (run_avg / 1e3) / 1e9
+    e2e_ms, h2d, d2h = time_e2e(wl, max(3, args.steps // 2), 2)
+    e2e_step = e2e_ms / max(3, args.steps // 2)
+    extra = {}
+    if rank == 0 and ws == 1 and not args.no_extra:
+        extra = mixed_vs_binned(max(5, args.steps // 2), 3)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(args.workload, budget_s=15.0)
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "GB/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "desc": spec["desc"], "batch": int(len(wl.lens)),
+                   "sum_kv_len": int(wl.lens.sum()), "kv_bytes_per_step": wl.bytes_kv,
+                   "num_q_heads": wl.shape.num_q_heads, "num_kv_heads": wl.shape.num_kv_heads, "head_dim": 128,
+                   "page_size": 16, "page_layout": "fragmented (seeded permutation)",
+                   "l2": "inputs larger than L2 (KV working set >> 126 MB); no flush",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single instance",
+                   "plan": {"items": info.num_items, "chunk_pages": info.chunk_pages, "ctas": info.num_ctas}},
+        "tokens_per_s": round(ws * len(wl.lens) / (ms_step / 1e3), 1),
+        "pct_hbm_peak": round(100.0 * value / (ws * peak), 2),
+        "roofline": {"bound": "hbm", "kernel": "decode_kernel (l4_decode_run)", "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": peak_src, "launch_ms": round(run_avg, 5),
+                     "bytes_per_launch": wl.bytes_algo},
+        "e2e": {"value": round(ws * wl.bytes_kv / (e2e_step / 1e3) / 1e9, 1), "unit": "GB/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_step, 5)},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk,
+    }
+    if cpu:
+        line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if extra:
+        line["extra"] = extra
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,214 @@
+"""GPU parity tests: l4_decode_attention (CUDA, sm_100a, through the C ABI) vs
+the FP64 oracle on the same seeded inputs.  Tolerance: max abs error 2e-3 on
+fp32 outputs (BASELINE.json north star); LSE within 2e-3 as well.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import attention as oa
+from paper_2512_19179_b200 import l4
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.init()
+
+
+def _to_dev(table, q, k, v):
+    d = "cuda"
+    return (q.to(d), k.to(d), v.to(d), torch.from_numpy(table.indptr).to(d), torch.from_numpy(table.indices).to(d),
+            torch.from_numpy(table.kv_len).to(d))
+
+
+def _run_gpu(table, q, k, v, **kw):
+    qd, kd, vd, ip, ix, kl = _to_dev(table, q, k, v)
+    out, lse = l4.decode_attention(qd, kd, vd, ip, ix, kl, **kw)
+    torch.cuda.synchronize()
+    return out.double().cpu().numpy(), lse.double().cpu().numpy()
+
+
+def _check(out, lse, ref_out, ref_lse, tol=TOL):
+    err = np.max(np.abs(out - ref_out)) if out.size else 0.0
+    assert err <= tol, f"max abs err {err}"
+    fin = np.isfinite(ref_lse)
+    assert np.all(np.isneginf(lse[~fin]))
+    if fin.any():
+        lerr = np.max(np.abs(lse[fin] - ref_lse[fin]))
+        assert lerr <= tol, f"lse err {lerr}"
+    return err
+
+
+def _case(lens, Hq, Hkv, seed=0, q_scale=1.0, spare=3, layout="fragmented"):
+    shape = synth.AttnShape("t", Hq, Hkv)
+    table = synth.make_page_table(np.asarray(lens), seed=seed, spare_pages=spare, layout=layout)
+    q, k, v = synth.make_qkv_cpu(shape, table, seed=seed, q_scale=q_scale, poison_unused=True)
+    ref_out, ref_lse = oa.paged_decode_attention(q, k, v, table.indptr, table.indices, table.kv_len, Hkv)
+    return shape, table, q, k, v, ref_out, ref_lse
+
+
+def test_c1_config():
+    """BASELINE.json configs[0]: 8 q / 2 kv heads, B=4, L = {16, 64, 256, 1024}."""
+    shape, table, q, k, v, ro, rl = _case(synth.lengths_c1(), 8, 2)
+    out, lse = _run_gpu(table, q, k, v)
+    err = _check(out, lse, ro, rl)
+    assert err < 1e-4
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("chunk", [0, -1, 1, 3])
+def test_random_shapes(G, chunk):
+    rng = np.random.default_rng(100 + G * 10 + chunk)
+    lens = [0, 1, 15, 16, 17, 31, 33, 100, 255, 256, 257, 1000] + rng.integers(1, 3000, size=6).tolist()
+    Hkv = 2 if G == 8 else 3
+    shape, table, q, k, v, ro, rl = _case(lens, Hkv * G, Hkv, seed=G)
+    out, lse = _run_gpu(table, q, k, v, chunk_pages=chunk)
+    _check(out, lse, ro, rl)
+
+
+def test_peaked_softmax():
+    """q x 4 makes the softmax peaked (adversarial for the probability precision, Z23)."""
+    shape, table, q, k, v, ro, rl = _case([16, 64, 256, 1024, 3000], 32, 8, seed=5, q_scale=4.0)
+    for chunk in (0, 2):
+        out, lse = _run_gpu(table, q, k, v, chunk_pages=chunk)
+        _check(out, lse, ro, rl)
+
+
+def test_bf16_output():
+    shape, table, q, k, v, ro, rl = _case([5, 77, 400, 2048], 16, 4, seed=9)
+    out, lse = _run_gpu(table, q, k, v, out_dtype=l4.L4_DT_BF16)
+    # bf16 rounding of the output adds up to 2^-9 relative (Z22)
+    assert np.max(np.abs(out - ro) - np.abs(ro) * 2.0 ** -8) <= TOL
+    _check(out * 0, lse, ro * 0, rl)
+
+
+def test_split_invariance_and_repeat_runs():
+    """Unsplit vs split at several chunk sizes agree; repeated runs with one plan are bit-identical."""
+    shape, table, q, k, v, ro, rl = _case([1, 40, 700, 5000], 32, 8, seed=3)
+    base, base_lse = _run_gpu(table, q, k, v, chunk_pages=-1)
+    for chunk in (1, 2, 7, 64):
+        out, lse = _run_gpu(table, q, k, v, chunk_pages=chunk)
+        assert np.max(np.abs(out - base)) < 2e-5
+        assert np.max(np.abs(lse - base_lse)[np.isfinite(base_lse)]) < 2e-5
+    qd, kd, vd, ip, ix, kl = _to_dev(table, q, k, v)
+    params = l4.make_params(table.batch, 32, 8, chunk_pages=2)
+    ws = l4.alloc_workspace(params, table.total_pages)
+    l4.decode_plan(params, kl, ip, table.total_pages, ws)
+    outs = []
+    for _ in range(3):
+        o = torch.empty(table.batch, 32, 128, device="cuda")
+        lz = torch.empty(table.batch, 32, device="cuda")
+        l4.decode_run(params, qd, kd, vd, ix, o, lz, ws)
+        outs.append((o.cpu(), lz.cpu()))
+    torch.cuda.synchronize()
+    for o, lz in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(lz, outs[0][1])
+
+
+def test_page_layout_independence_bitwise():
+    lens = [16, 100, 513, 2000]
+    shape, t1, q, k, v, ro, rl = _case(lens, 16, 4, seed=4, layout="contiguous", spare=0)
+    out1, lse1 = _run_gpu(t1, q, k, v)
+    perm = np.random.default_rng(1).permutation(t1.num_pages)
+    k2 = torch.empty_like(k)
+    v2 = torch.empty_like(v)
+    k2[torch.as_tensor(perm)] = k
+    v2[torch.as_tensor(perm)] = v
+    t2 = synth.PageTable(kv_len=t1.kv_len, indptr=t1.indptr, indices=perm[t1.indices].astype(np.int32),
+                         num_pages=t1.num_pages)
+    out2, lse2 = _run_gpu(t2, q, k2, v2)
+    assert np.array_equal(out1, out2) and np.array_equal(lse1, lse2)
+
+
+def test_plan_covers_every_token_once():
+    rng = np.random.default_rng(11)
+    lens = np.concatenate([[0, 1, 16, 17], rng.integers(1, 20000, size=60), [131072]])
+    table = synth.make_page_table(lens, seed=0)
+    kl = torch.from_numpy(table.kv_len).cuda()
+    ip = torch.from_numpy(table.indptr).cuda()
+    for chunk in (0, 5):
+        params = l4.make_params(table.batch, 32, 8, chunk_pages=chunk)
+        ws = l4.alloc_workspace(params, table.total_pages)
+        l4.decode_plan(params, kl, ip, table.total_pages, ws)
+        items = l4.plan_items(ws)
+        info = l4.plan_info(ws)
+        assert info.num_items == len(items)
+        covered = {}
+        sizes = []
+        for b, h, pb, pe, last_valid, part_base, ns, s in items.tolist():
+            L = int(table.kv_len[b])
+            base = int(table.indptr[b])
+            npg = (L + 15) // 16
+            assert base <= pb <= pe <= base + npg
+            if L > 0:
+                assert pe > pb
+            for p in range(pb, pe):
+                key = (b, h, p)
+                assert key not in covered
+                covered[key] = 1
+            if pe == base + npg and L > 0:
+                assert last_valid == L - (npg - 1) * 16
+            sizes.append(pe - pb)
+        expect = sum(8 * ((int(L) + 15) // 16) for L in table.kv_len)
+        assert len(covered) == expect
+        # length-binned, longest bin first: bit_length of item size is non-increasing
+        bl = [int(x).bit_length() for x in sizes]
+        assert all(a >= b for a, b in zip(bl, bl[1:]))
+
+
+def test_empty_batch_and_all_empty_requests():
+    shape, table, q, k, v, ro, rl = _case([0, 0, 0], 8, 2)
+    out, lse = _run_gpu(table, q, k, v)
+    assert np.all(out == 0) and np.all(np.isneginf(lse))
+    params = l4.make_params(0, 8, 2)
+    assert l4.lib().l4_decode_plan(params, None, None, 0, None, 0, None) == 0
+
+
+def _sampled_full_size(lens, shape, seed, samples):
+    """Full-size parity in the bench launch configuration (auto plan), on sampled requests."""
+    table = synth.make_page_table(lens, seed=seed, spare_pages=64)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    B = table.batch
+    q = torch.randn(B, shape.num_q_heads, 128, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(table.num_pages, shape.num_kv_heads, 16, 128, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(table.num_pages, shape.num_kv_heads, 16, 128, device="cuda", generator=g).to(torch.bfloat16)
+    ip = torch.from_numpy(table.indptr).cuda()
+    ix = torch.from_numpy(table.indices).cuda()
+    kl = torch.from_numpy(table.kv_len).cuda()
+    out, lse = l4.decode_attention(q, k, v, ip, ix, kl)
+    torch.cuda.synchronize()
+    ro, rl = oa.paged_decode_attention(q, k, v, table.indptr, table.indices, table.kv_len, shape.num_kv_heads,
+                                       requests=samples)
+    o = out.double().cpu().numpy()
+    lz = lse.double().cpu().numpy()
+    err = max(np.max(np.abs(o[b] - ro[b])) for b in samples)
+    lerr = max(np.max(np.abs(lz[b] - rl[b])) for b in samples)
+    assert err <= TOL and lerr <= TOL, (err, lerr)
+    assert torch.isfinite(out).all()
+    return err
+
+
+def test_full_size_c2_sampled():
+    lens = synth.lengths_c2()
+    _sampled_full_size(lens, synth.SHAPE_LLAMA3_8B, 0, [0, 1, 124, 249])
+
+
+def test_full_size_c3_sampled():
+    lens = synth.lengths_c3(0)
+    order = np.argsort(lens)
+    samples = sorted(set([int(order[0]), int(order[1]), int(order[128]), int(order[-2]), int(order[-1])]))
+    _sampled_full_size(lens, synth.SHAPE_LLAMA3_8B, 0, samples)
+
+
+def test_full_size_c4_sampled():
+    lens = synth.lengths_c4(0)
+    _sampled_full_size(lens, synth.SHAPE_LLAMA3_70B, 0, [0, 31])

@@ -1,0 +1,178 @@
+"""CPU tests of the native library (no GPU needed): the C ABI loads and exports
+every symbol include/l4.h declares; l4_partition is bit-exact with the oracle;
+l4_pool_* matches the oracle allocator; argument validation."""
+import math
+import os
+import re
+import time
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import partition as op
+from oracle import pool as opool
+from paper_2512_19179_b200 import l4
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "l4.h")).read()
+    declared = set(re.findall(r"\b(l4_[a-z0-9_]+)\s*\(", hdr))
+    assert len(declared) >= 20
+    L = l4.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert declared == set(l4.EXPORTED_SYMBOLS)
+    assert "sm_100a" in l4.version()
+
+
+def _both(I, O, E, D, bw, kvb, edges=None, mode=0, chain=False):
+    try:
+        ref = op.plan_dp(I, O, E, D, bw, kvb, edges=edges, mode=mode, chain=chain)
+        ref_err = None
+    except op.InvalidArgument:
+        ref, ref_err = None, l4.L4_ERR_INVALID_ARG
+    except op.Infeasible:
+        ref, ref_err = None, l4.L4_ERR_INFEASIBLE
+    try:
+        got = l4.partition(I, O, E, D, bw, kvb, edges=edges, mode=mode, chain=chain)
+        got_err = None
+    except l4.L4Error as e:
+        got, got_err = None, e.status
+    return ref, ref_err, got, got_err
+
+
+def test_partition_bit_exact_random():
+    rng = np.random.default_rng(123)
+    for case in range(120):
+        n = int(rng.integers(0, 60))
+        I = rng.integers(1, int(rng.choice([20, 600, 5000])), size=n).tolist()
+        O = rng.integers(1, int(rng.choice([20, 600, 5000])), size=n).tolist()
+        D = tuple(float(x) for x in rng.random(5) * np.array([1e-2, 1e-4, 1e-6, 1e-9, 1e-5]))
+        E = int(rng.integers(1, 9))
+        bw = float(rng.uniform(1e3, 1e9))
+        kvb = int(rng.integers(0, 200000))
+        for mode in (0, 1):
+            for chain in (False, True):
+                ref, ref_err, got, got_err = _both(I, O, E, D, bw, kvb, mode=mode, chain=chain)
+                assert ref_err == got_err
+                if ref is None:      # chain with E > buckets: infeasible on both sides
+                    continue
+                assert got[0] == ref[0], (case, mode, chain)
+                assert got[1] == ref[1]            # bitwise-identical objective (Z14)
+
+
+def test_partition_bit_exact_custom_edges_and_errors():
+    I, O = [3, 9, 14], [2, 5, 1]
+    cases = [
+        dict(edges=[0, 4, 8, 16]), dict(edges=[0, 16]), dict(edges=[0, 2, 3, 5, 8, 13, 21]),
+        dict(edges=[0, 4, 8]),            # 9+5 = 14 uncovered -> infeasible
+        dict(edges=[0, 4, 4, 16]),        # not increasing -> invalid
+        dict(edges=[1, 4, 16]),           # must start at 0 -> invalid
+    ]
+    for kw in cases:
+        for E in (1, 2, 3):
+            ref, ref_err, got, got_err = _both(I, O, E, (0.1, 0.2, 0.3, 0.4, 0.5), 10.0, 3, **kw)
+            assert ref_err == got_err, kw
+            if ref is not None:
+                assert got == ref
+    for bad in [dict(E=0), dict(bw=0.0), dict(I=[0])]:
+        E = bad.get("E", 2)
+        ref, ref_err, got, got_err = _both(bad.get("I", [1]), [1], E, (1,) * 5, bad.get("bw", 1.0), 1)
+        assert ref_err == got_err == l4.L4_ERR_INVALID_ARG
+
+
+def test_partition_golden_examples():
+    import json
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "partition_examples.json")))
+    for ex in gold["plans"]:
+        stages, obj = l4.partition(ex["I"], ex["O"], ex["E"], ex["D"], ex["bandwidth"], ex["kv_bytes_per_token"],
+                                   mode=ex["mode"])
+        assert obj == ex["objective"]
+        if "stages" in ex:
+            assert [list(s) for s in stages] == ex["stages"]
+
+
+def test_partition_sharegpt_scale_bit_exact():
+    I, O = synth.requests_sharegpt_like(seed=0, n=2000)
+    D = synth.roofline_qoe_d()
+    for E in (2, 4, 8):
+        for mode in (0, 1):
+            ref = op.plan_dp(I, O, E, D, 7e11, 131072, mode=mode)
+            got = l4.partition(I, O, E, D, 7e11, 131072, mode=mode)
+            assert got[0] == ref[0] and got[1] == ref[1]
+
+
+def test_partition_speed_paper_setting():
+    """E = 16 over a 128K-context trace in 0.06 s; S:685 relaxes to < 1 s."""
+    I, O = synth.requests_sharegpt_like(seed=1, n=10000)
+    D = synth.roofline_qoe_d()
+    t = time.perf_counter()
+    stages, obj = l4.partition(I, O, 16, D, 7e11, 131072, mode=0)
+    dt = time.perf_counter() - t
+    assert dt < 1.0
+    assert sum(m for _, _, m in stages) == 16 and math.isfinite(obj)
+
+
+def test_pool_matches_oracle_random_ops():
+    rng = np.random.default_rng(7)
+    N = 300
+    ref = opool.PagePool(N)
+    got = l4.PagePool(N)
+    owned = []
+    for step in range(3000):
+        r = rng.random()
+        if owned and r < 0.4:
+            k = int(rng.integers(len(owned)))
+            pages = owned.pop(k)
+            ref.release(pages)
+            got.free(pages)
+        elif r < 0.45 and owned:
+            # double free / bad free must fail identically without side effects
+            pages = list(owned[int(rng.integers(len(owned)))]) + [int(rng.integers(N))]
+            pages = pages + pages[:1]
+            with pytest.raises(opool.InvalidFree):
+                ref.release(pages)
+            with pytest.raises(l4.L4Error) as ei:
+                got.free(pages)
+            assert ei.value.status == l4.L4_ERR_INVALID_ARG
+        else:
+            n = int(rng.integers(0, 40))
+            try:
+                rp = ref.alloc(n)
+            except opool.NoPages:
+                rp = None
+            if rp is None:
+                with pytest.raises(l4.NoPagesError):
+                    got.alloc(n)
+            else:
+                gp = got.alloc(n)
+                assert gp.tolist() == rp
+                owned.append(rp)
+        assert got.num_free() == ref.num_free()
+
+
+def test_decode_without_gpu_fails_loudly():
+    """No CPU fallback: on a host without a B200 the device calls return L4_ERR_CUDA."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = l4.make_params(4, 8, 2)
+    n = l4.lib().l4_decode_workspace_size(p, 100)
+    assert n == 0
+    assert "cuda" in l4.lib().l4_last_error().decode().lower() or "device" in l4.lib().l4_last_error().decode().lower()
+
+
+def test_decode_param_validation():
+    L = l4.lib()
+    for kw, status in [(dict(head_dim=64), l4.L4_ERR_UNSUPPORTED), (dict(page_size=32), l4.L4_ERR_UNSUPPORTED),
+                       (dict(num_q_heads=12, num_kv_heads=8), l4.L4_ERR_INVALID_ARG),
+                       (dict(num_q_heads=48, num_kv_heads=3), l4.L4_ERR_UNSUPPORTED),
+                       (dict(batch=-1), l4.L4_ERR_INVALID_ARG)]:
+        args = dict(batch=4, num_q_heads=8, num_kv_heads=2, head_dim=128, page_size=16)
+        args.update(kw)
+        p = l4.make_params(**args)
+        st = L.l4_decode_plan(p, None, None, 0, None, 0, None)
+        assert st == status, (kw, st, L.l4_last_error())
