@@ -6,24 +6,27 @@
 // every request b and q-head h, softmax(scale * q K^T) V over the L_b cached
 // tokens of kv head h/G, plus the natural-log LSE.
 //
-// How (B200 design, DESIGN.md §Kernels):
-//  a1  plan_kernel (1 CTA): pages -> chunk size C -> near-equal splits per
-//      request -> items binned by chunk length, longest bin first (LPT), so the
-//      longest request's splits start first and short requests fill the tail
-//      (the paper's inter-SM imbalance).  Zeroes split counters.
-//  a2  decode_kernel (persistent, 1 producer + 4 consumer warps per CTA):
-//      the producer warp streams each (page, kv head) K and V slice (4 KB each,
-//      HND layout) with TMA (cp.async.bulk.tensor, 128B swizzle, L2
-//      evict-first) into an 8-stage shared-memory ring tracked by mbarriers;
-//      consumer warps compute S^T = K Q^T and O^T += V^T P^T with mma.sync
-//      m16n8k16 (tokens / head_dim on the M side, the G <= 8 query heads on
-//      the N side, so GQA group 8 has no padding), an online softmax with
-//      warp-shuffle max reductions in the exp2 domain, and P split into
-//      bf16 hi + lo (reading Z23) so the probability rounding stays < 1e-5.
+// How (B200 design, DESIGN.md §4):
+//  a1  plan_kernel (1 CTA): pages -> chunk size C -> near-equal splits of the
+//      requests longer than 2C -> work items binned by split length, longest
+//      bin first (LPT order), so the longest request's splits start first and
+//      short requests fill the tail (the paper's inter-SM imbalance and
+//      partitioning inefficiency).  Zeroes the split counters and
+//      the dynamic scheduler.
+//  a2  decode_kernel (persistent, 1 producer + 4 consumer warps per CTA,
+//      2 CTAs per SM): items are handed out dynamically (first one static,
+//      then an atomic ticket), so CTAs that finish early take the next-largest
+//      item.  The producer warp streams each (page, kv head) K and V slice
+//      (4 KB each, HND layout) with one TMA each (cp.async.bulk.tensor, 128B
+//      swizzle, L2 evict-first) into an 8-stage shared-memory ring tracked by
+//      mbarriers; consumer warps compute S^T = K Q^T and O^T += V^T P^T with
+//      mma.sync m16n8k16 (tokens / head_dim on M, the G <= 8 query heads on N,
+//      so GQA group 8 has no padding), an online softmax with warp-shuffle max
+//      reductions in the exp2 domain, and P split into bf16 hi + lo (Z23).
 //  a3  LSE combine: the 4 warps of a CTA merge their (m, l, O) in shared
 //      memory; a split item writes (O/l, lse) to the workspace and the last
-//      split to finish for (b, kv head) (atomic counter) combines all splits
-//      (FlashDecoding aggregation) — no second kernel launch.
+//      split of (b, kv head) to finish (acq_rel atomic ticket) combines all
+//      splits (FlashDecoding aggregation) — no second launch.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -44,17 +47,20 @@ namespace {
 constexpr int kPage = 16;
 constexpr int kHeadDim = 128;
 constexpr int kConsumerWarps = 4;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;  // 160
+constexpr int kConsumerThreads = kConsumerWarps * 32;
+constexpr int kThreads = kConsumerThreads + 32;      // + 1 producer warp = 160
 constexpr int kStages = 8;
-constexpr int kTileBytes = kPage * 64 * 2;            // 16 rows x 64 bf16 = 2 KB (one 128B-swizzle box)
-constexpr int kStageBytes = 4 * kTileBytes;           // K[0:64], K[64:128], V[0:64], V[64:128]
+constexpr int kSliceBytes = kPage * kHeadDim * 2;     // one (page, kv head) K or V slice = 4 KB
+constexpr int kHalfBytes = kSliceBytes / 2;           // 16 rows x 64 bf16 (128 B swizzle span)
+constexpr int kStageBytes = 2 * kSliceBytes;          // K, V
 constexpr int kItemSlots = 4;
 constexpr int kMaxG = 8;
 constexpr int kQSlotBytes = kMaxG * kHeadDim * 2;     // 2 KB
 constexpr int kMergeStride = kHeadDim + 4;            // floats per head row (bank-conflict padding)
 constexpr int kMaxSplits = 512;                       // per (request, kv head); lse staging capacity
 constexpr int kMinChunk = 8;                          // pages
-constexpr int kItemsPerCta = 8;                       // auto chunk target
+constexpr int kItemsPerCta = 8;                       // automatic chunk target
+constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
 constexpr int kNumBins = 32;
@@ -66,12 +72,14 @@ struct __align__(16) WorkItem {
 };
 static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
 
+// Header region (256 B): plan summary + dynamic scheduler state.
 struct __align__(16) PlanHeader {
   int n_items, chunk, num_ctas, max_splits;
   int batch, num_kv_heads, items_cap, pad;
   int pad2[8];
+  int sched_next, sched_done, pad3[14];  // ticket counter and finished-CTA count (self-resetting)
 };
-static_assert(sizeof(PlanHeader) == 64, "PlanHeader is 64 bytes");
+static_assert(sizeof(PlanHeader) == 128, "PlanHeader is 128 bytes");
 
 // ------------------------------------------------------------------ workspace layout
 struct WsLayout {
@@ -107,7 +115,6 @@ bool ws_layout_from_bytes(int B, int Hkv, int G, size_t bytes, WsLayout* out) {
   return true;
 }
 
-// ------------------------------------------------------------------ device info cache
 l4_status get_device(int* dev_out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -119,8 +126,6 @@ l4_status get_device(int* dev_out) {
   *dev_out = dev;
   return L4_OK;
 }
-
-int num_ctas_for(int sms, int occ) { return sms * std::max(1, std::min(occ, 2)); }
 
 // ------------------------------------------------------------------ parameter checks
 l4_status check_params(const l4_decode_params* p, int* G_out) {
@@ -141,7 +146,7 @@ l4_status check_params(const l4_decode_params* p, int* G_out) {
 
 int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// items_cap: upper bound on work items for any batch with <= max_total_pages pages.
+// Upper bound on work items for any batch with <= max_total_pages pages.
 int items_cap_for(const l4_decode_params* p, int64_t max_total_pages, int num_ctas) {
   const int64_t B = p->batch, Hkv = p->num_kv_heads;
   int64_t cap;
@@ -150,6 +155,7 @@ int items_cap_for(const l4_decode_params* p, int64_t max_total_pages, int num_ct
   } else if (p->chunk_pages > 0) {
     cap = Hkv * (B + ceil_div64(max_total_pages, p->chunk_pages));
   } else {
+    // C >= T*Hkv/(W*k) => Hkv * sum ceil(p_b / C) <= W*k + Hkv*B
     cap = std::min(Hkv * (B + ceil_div64(max_total_pages, kMinChunk)),
                    Hkv * B + (int64_t)num_ctas * kItemsPerCta + Hkv);
   }
@@ -176,8 +182,7 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
   return v;
 }
 
-// Block-wide exclusive scan of one int per thread (1024 threads); returns the
-// exclusive prefix and the block total.
+// Block-wide exclusive scan of one int per thread (1024 threads).
 __device__ int block_excl_scan(int v, int* total, int* s_warp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int incl = warp_incl_scan(v);
@@ -195,32 +200,32 @@ __device__ int block_excl_scan(int v, int* total, int* s_warp) {
   return s_warp[warp] + incl - v;
 }
 
-__device__ long long block_sum_ll(long long v, long long* s) {
+// Block-wide sum (int64) and max (int) in one pass.
+__device__ void block_sum_max(long long v, int m, long long* s_ll, int* s_i, long long* sum_out, int* max_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 16; o; o >>= 1) {
+    v += __shfl_xor_sync(0xffffffffu, v, o);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
   __syncthreads();
-  if (lane == 0) s[warp] = v;
+  if (lane == 0) {
+    s_ll[warp] = v;
+    s_i[warp] = m;
+  }
   __syncthreads();
   long long t = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s[i];
-  return t;
-}
-
-__device__ int block_max_i(int v, int* s) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();
-  if (lane == 0) s[warp] = v;
-  __syncthreads();
-  int t = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = max(t, s[i]);
-  return t;
+  int mm = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    t += s_ll[i];
+    mm = max(mm, s_i[i]);
+  }
+  *sum_out = t;
+  *max_out = mm;
 }
 
 __device__ __forceinline__ int nsplit_of(int pages, long long C) {
-  if (pages <= 0) return 1;
+  if (pages <= (long long)kNoSplitFactor * C) return 1;  // also pages == 0
   return (int)((pages + C - 1) / C);
 }
 
@@ -233,13 +238,25 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
 constexpr int kPlanMaxR = kMaxBatch / kPlanThreads;  // requests per thread
 
 __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
-  extern __shared__ int plan_smem[];          // s_off[B], s_b[B] (binned order)
-  int* s_off = plan_smem;
-  int* s_b = plan_smem + max(a.B, 1);
+  // PDL: let the dependent decode kernel start its prologue now; it waits
+  // (griddepcontrol.wait) for this grid's completion before reading the plan.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ int plan_smem[];  // s_len[B], s_ptr[B], s_off[B], s_b[B]
+  const int Bs = max(a.B, 1);
+  int* s_len = plan_smem;
+  int* s_ptr = plan_smem + Bs;
+  int* s_off = plan_smem + 2 * Bs;
+  int* s_b = plan_smem + 3 * Bs;
   __shared__ long long s_ll[32];
   __shared__ int s_i[33];
   __shared__ int s_hist[kNumBins];
   const int tid = threadIdx.x;
+  for (int b = tid; b < a.B; b += kPlanThreads) {
+    s_len[b] = a.kv_len[b];
+    s_ptr[b] = a.indptr[b];
+  }
+  if (tid < kNumBins) s_hist[tid] = 0;
+  __syncthreads();
   const int R = (a.B + kPlanThreads - 1) / kPlanThreads;
 
   int pages[kPlanMaxR];
@@ -250,15 +267,16 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     const int b = tid * R + r;
     int pg = 0;
     if (r < R && b < a.B) {
-      const int L = a.kv_len[b];
+      const int L = s_len[b];
       pg = L > 0 ? (L + kPage - 1) / kPage : 0;
     }
     pages[r] = pg;
     my_sum += pg;
     my_max = max(my_max, pg);
   }
-  const long long T = block_sum_ll(my_sum, s_ll);
-  const int Pmax = block_max_i(my_max, s_i);
+  long long T;
+  int Pmax;
+  block_sum_max(my_sum, my_max, s_ll, s_i, &T, &Pmax);
 
   // chunk size C (pages per work item)
   long long C;
@@ -277,14 +295,13 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
 #pragma unroll
     for (int r = 0; r < kPlanMaxR; ++r)
       if (r < R && tid * R + r < a.B) my_items += (long long)nsplit_of(pages[r], C) * a.Hkv;
-    N = block_sum_ll(my_items, s_ll);
+    int dummy;
+    block_sum_max(my_items, 0, s_ll, s_i, &N, &dummy);
     if (N <= a.items_cap) break;
     C *= 2;
   }
 
   // ---- length bins, longest first (stable by request index within a bin)
-  if (tid < kNumBins) s_hist[tid] = 0;
-  __syncthreads();
   int bins[kPlanMaxR];
 #pragma unroll
   for (int r = 0; r < kPlanMaxR; ++r) {
@@ -303,6 +320,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
         my_cnt += nsplit_of(pages[r], C) * a.Hkv;
         my_n += 1;
       }
+    // one scan of (items << 16 | requests) would overflow; do two small scans
     int tot_items, tot_n;
     const int ex_items = block_excl_scan(my_cnt, &tot_items, s_i);
     const int ex_n = block_excl_scan(my_n, &tot_n, s_i);
@@ -329,24 +347,20 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
       if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
     }
     const int b = s_b[lo];
-    const int L = a.kv_len[b];
+    const int L = s_len[b];
     const int pg = L > 0 ? (L + kPage - 1) / kPage : 0;
     const int ns = nsplit_of(pg, C);
     const int local = i - s_off[lo];
     const int h = local / ns, s = local - h * ns;
     const int p0 = (int)(((long long)s * pg) / ns);
     const int p1 = (int)(((long long)(s + 1) * pg) / ns);
-    const int base = a.indptr[b];
-    WorkItem it;
-    it.b = b;
-    it.h = h;
-    it.pbeg = base + p0;
-    it.pend = base + p1;
-    it.last_valid = (p1 == pg && pg > 0) ? (L - (pg - 1) * kPage) : (p1 > p0 ? kPage : 0);
-    it.part_base = s_off[lo] + h * ns;
-    it.nsplit = ns;
-    it.split = s;
-    a.items[i] = it;
+    const int base = s_ptr[b];
+    int4 w0 = make_int4(b, h, base + p0, base + p1);
+    int4 w1 = make_int4((p1 == pg && pg > 0) ? (L - (pg - 1) * kPage) : (p1 > p0 ? kPage : 0),
+                        s_off[lo] + h * ns, ns, s);
+    int4* dst = reinterpret_cast<int4*>(a.items + i);
+    dst[0] = w0;
+    dst[1] = w1;
   }
   for (int i = tid; i < a.B * a.Hkv; i += kPlanThreads) a.counters[i] = 0;
   if (tid == 0) {
@@ -359,6 +373,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     hd.batch = a.B;
     hd.num_kv_heads = a.Hkv;
     hd.items_cap = a.items_cap;
+    hd.sched_next = 0;
+    hd.sched_done = 0;
     *a.header = hd;
   }
 }
@@ -370,7 +386,7 @@ struct RunArgs {
   float* lse;
   const int* indices;
   const WorkItem* items;
-  const PlanHeader* header;
+  PlanHeader* header;
   int* counters;
   float* part_o;
   float* part_lse;
@@ -379,11 +395,16 @@ struct RunArgs {
   int out_bf16;
 };
 
+struct __align__(16) SlotItem {  // item handed from the producer to the consumers
+  WorkItem it;
+  int idx, pad[3];
+};
+
 struct SmemLayout {
   static constexpr int stages = 0;
   static constexpr int qslots = stages + kStages * kStageBytes;
   static constexpr int items = qslots + kItemSlots * kQSlotBytes;
-  static constexpr int merge_o = items + kItemSlots * (int)sizeof(WorkItem);
+  static constexpr int merge_o = items + kItemSlots * (int)sizeof(SlotItem);
   static constexpr int merge_m = merge_o + kConsumerWarps * kMaxG * kMergeStride * 4;
   static constexpr int merge_l = merge_m + kConsumerWarps * kMaxG * 4;
   static constexpr int bars = merge_l + kConsumerWarps * kMaxG * 4;
@@ -401,6 +422,18 @@ __device__ __forceinline__ void store_out(const RunArgs& a, size_t idx, float v)
     reinterpret_cast<float*>(a.out)[idx] = v;
 }
 
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Byte offset of 16-B chunk cd (0..15) of token t in a staged slice: two
+// 16-row x 128-B halves (d 0..63, d 64..127), 128-byte swizzle (chunk ^= row % 8).
+__device__ __forceinline__ uint32_t slice_off(int t, int cd) {
+  return (uint32_t)((cd >> 3) * kHalfBytes + t * 128 + (((cd & 7) ^ (t & 7)) << 4));
+}
+
 // One page (16 tokens) of one (request, kv head): S^T = K Q^T, online softmax, O^T += V^T P^T.
 __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const uint32_t (&qf)[8][2],
                                              float (&acc)[8][4], float (&mrow)[2], float (&lrow)[2],
@@ -413,13 +446,10 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
   float s[4] = {0.f, 0.f, 0.f, 0.f};
   {
     const int tok = r8 + ((mi & 1) << 3);
-    const uint32_t row = sbase + tok * 128;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const int cd = kk * 2 + (mi >> 1);  // 16-B chunk 0..15 of the 256-B row
-      const uint32_t addr = row + (cd >> 3) * kTileBytes + (((cd & 7) ^ r8) << 4);
       uint32_t a0, a1, a2, a3;
-      ldmatrix_x4(addr, a0, a1, a2, a3);
+      ldmatrix_x4(sbase + slice_off(tok, kk * 2 + (mi >> 1)), a0, a1, a2, a3);
       mma_bf16_16816(s, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
     }
   }
@@ -459,16 +489,14 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
   // ---- O^T[128 d x 8 heads] += V^T[128 x 16 tok] * P^T[16 tok x 8 heads]
   {
     const int tok = r8 + ((mi >> 1) << 3);
-    const uint32_t row = sbase + 2 * kTileBytes + tok * 128;
+    const uint32_t vbase = sbase + kSliceBytes;
     // masks for invalid tokens of a partial last page (V may hold NaN there)
     const uint32_t mlo = (((2 * c) < valid) ? 0x0000ffffu : 0u) | (((2 * c + 1) < valid) ? 0xffff0000u : 0u);
     const uint32_t mhi = (((2 * c + 8) < valid) ? 0x0000ffffu : 0u) | (((2 * c + 9) < valid) ? 0xffff0000u : 0u);
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
-      const int cd = mt * 2 + (mi & 1);
-      const uint32_t addr = row + (cd >> 3) * kTileBytes + (((cd & 7) ^ r8) << 4);
       uint32_t a0, a1, a2, a3;
-      ldmatrix_x4_trans(addr, a0, a1, a2, a3);
+      ldmatrix_x4_trans(vbase + slice_off(tok, mt * 2 + (mi & 1)), a0, a1, a2, a3);
       if (valid < kPage) {
         a0 &= mlo;
         a1 &= mlo;
@@ -481,22 +509,36 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
   }
 }
 
+__device__ __forceinline__ WorkItem load_item(const WorkItem* items, int i, int n) {
+  WorkItem it;
+  if (i < n) {
+    const int4* p = reinterpret_cast<const int4*>(items + i);
+    const int4 x = __ldg(p), y = __ldg(p + 1);
+    it.b = x.x; it.h = x.y; it.pbeg = x.z; it.pend = x.w;
+    it.last_valid = y.x; it.part_base = y.y; it.nsplit = y.z; it.split = y.w;
+  } else {
+    it.b = -1; it.h = 0; it.pbeg = 0; it.pend = 0; it.last_valid = 0; it.part_base = 0; it.nsplit = 1; it.split = 0;
+  }
+  return it;
+}
+
 template <int G>
 __global__ void __launch_bounds__(kThreads, 2)
     decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, RunArgs a) {
   using namespace dev;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  unsigned char* smem = smem_raw + ((1024u - (raw_u32 & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase + SmemLayout::bars;
   const uint32_t bar_empty = bar_full + kStages * 8;
   const uint32_t bar_ifull = bar_empty + kStages * 8;
   const uint32_t bar_iempty = bar_ifull + kItemSlots * 8;
-  WorkItem* s_items = reinterpret_cast<WorkItem*>(smem + SmemLayout::items);
+  SlotItem* s_items = reinterpret_cast<SlotItem*>(smem + SmemLayout::items);
   float* merge_o = reinterpret_cast<float*>(smem + SmemLayout::merge_o);
   float* merge_m = reinterpret_cast<float*>(smem + SmemLayout::merge_m);
   float* merge_l = reinterpret_cast<float*>(smem + SmemLayout::merge_l);
-  int* s_flag = reinterpret_cast<int*>(smem + SmemLayout::flag);
+  volatile int* s_flag = reinterpret_cast<volatile int*>(smem + SmemLayout::flag);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -510,43 +552,62 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     fence_mbar_init();
   }
+  if (warp == kConsumerWarps && lane == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+  }
   __syncthreads();
+  // PDL: everything above overlapped the planner; the plan is read below.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int n_items = a.header->n_items;
   const int W = gridDim.x;
 
   if (warp == kConsumerWarps) {
     // ============================== producer warp: items, Q and KV pages via TMA
-    if (lane == 0) {
-      prefetch_tmap(&tmK);
-      prefetch_tmap(&tmV);
-    }
     const uint64_t policy = policy_evict_first();
-    auto load_item = [&](int i) -> WorkItem {
-      WorkItem it;
-      if (i < n_items) {
-        const int4* p = reinterpret_cast<const int4*>(a.items + i);
-        int4 x = __ldg(p), y = __ldg(p + 1);
-        it.b = x.x; it.h = x.y; it.pbeg = x.z; it.pend = x.w;
-        it.last_valid = y.x; it.part_base = y.y; it.nsplit = y.z; it.split = y.w;
-      } else {
-        it.b = 0; it.h = 0; it.pbeg = 0; it.pend = 0; it.last_valid = 0; it.part_base = 0; it.nsplit = 1; it.split = 0;
+    bool exhausted = false;
+    // Dynamic LPT scheduling: the first item is blockIdx.x, later ones come from
+    // an atomic ticket (W + ticket) so idle CTAs take the next-largest item.
+    auto draw = [&]() -> int {
+      int idx = n_items;
+      if (!exhausted) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&a.header->sched_next, 1);
+        idx = W + __shfl_sync(0xffffffffu, t, 0);
+        if (idx >= n_items) {
+          exhausted = true;
+          idx = n_items;
+          if (lane == 0) {
+            const int done = atomicAdd(&a.header->sched_done, 1);
+            if (done == W - 1) {  // every CTA stopped drawing: reset for the next run
+              a.header->sched_next = 0;
+              a.header->sched_done = 0;
+            }
+          }
+        }
       }
-      return it;
+      return idx;
     };
-    int i = blockIdx.x;
-    WorkItem cur = load_item(i);
-    WorkItem nxt = load_item(i + W);
-    int cur_idx = (i < n_items && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
-    uint32_t k = 0;
-    uint32_t qseq = 0;
-    for (; i < n_items; i += W, ++k) {
-      const WorkItem nn = load_item(i + 2 * W);
-      const int nxt_idx = (i + W < n_items && lane < nxt.pend - nxt.pbeg) ? __ldg(a.indices + nxt.pbeg + lane) : 0;
+    int i_cur = blockIdx.x < n_items ? (int)blockIdx.x : n_items;
+    int i_nxt = draw();
+    WorkItem cur = load_item(a.items, i_cur, n_items);
+    WorkItem nxt = load_item(a.items, i_nxt, n_items);
+    int i_nn = draw();
+    int cur_idx = (i_cur < n_items && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
+    uint32_t k = 0, qseq = 0;
+    for (; i_cur < n_items; ++k) {
+      // prefetch: the next item's first page ids, the item after's struct, one more ticket
+      const int nxt_idx = (i_nxt < n_items && lane < nxt.pend - nxt.pbeg) ? __ldg(a.indices + nxt.pbeg + lane) : 0;
+      const WorkItem nn = load_item(a.items, i_nn, n_items);
+      const int i_nnn = draw();
       const uint32_t slot = k % kItemSlots;
       if (lane == 0) {
         mbar_wait(bar_iempty + slot * 8, ((k / kItemSlots) & 1) ^ 1);
-        s_items[slot] = cur;
+        SlotItem si;
+        si.it = cur;
+        si.idx = i_cur;
+        s_items[slot] = si;
         const uint32_t qbytes = G * kHeadDim * 2;
         mbar_arrive_expect_tx(bar_ifull + slot * 8, qbytes);
         bulk_load(sbase + SmemLayout::qslots + slot * kQSlotBytes,
@@ -566,18 +627,27 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_arrive_expect_tx(fb, kStageBytes);
             const int row = (page * a.Hkv + cur.h) * kPage;
             const uint32_t dst = sbase + SmemLayout::stages + st * kStageBytes;
-            tma_load_2d(dst, &tmK, 0, row, fb, policy);
-            tma_load_2d(dst + kTileBytes, &tmK, 64, row, fb, policy);
-            tma_load_2d(dst + 2 * kTileBytes, &tmV, 0, row, fb, policy);
-            tma_load_2d(dst + 3 * kTileBytes, &tmV, 64, row, fb, policy);
+            tma_load_3d(dst, &tmK, 0, row, 0, fb, policy);
+            tma_load_3d(dst + kSliceBytes, &tmV, 0, row, 0, fb, policy);
           }
           ++qseq;
         }
         blk = nb;
       }
+      i_cur = i_nxt;
       cur = nxt;
-      nxt = nn;
       cur_idx = nxt_idx;
+      i_nxt = i_nn;
+      nxt = nn;
+      i_nn = i_nnn;
+    }
+    while (!exhausted) draw();  // make sure this CTA is counted as done
+    // sentinel: tell the consumers there is no more work
+    if (lane == 0) {
+      const uint32_t slot = k % kItemSlots;
+      mbar_wait(bar_iempty + slot * 8, ((k / kItemSlots) & 1) ^ 1);
+      s_items[slot].it.b = -1;
+      mbar_arrive(bar_ifull + slot * 8);
     }
     return;
   }
@@ -585,12 +655,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   // ============================== consumer warps
   const int g = lane >> 2, c = lane & 3;
   const int ct = threadIdx.x;  // 0..127
-  uint32_t k = 0;
   uint32_t qbase = 0;
-  for (int i = blockIdx.x; i < n_items; i += W, ++k) {
+  for (uint32_t k = 0;; ++k) {
     const uint32_t slot = k % kItemSlots;
     mbar_wait(bar_ifull + slot * 8, (k / kItemSlots) & 1);
-    const WorkItem it = s_items[slot];
+    const WorkItem it = s_items[slot].it;
+    const int item_idx = s_items[slot].idx;
+    if (it.b < 0) break;
     uint32_t qf[8][2];
     {
       const unsigned char* qs = smem + SmemLayout::qslots + slot * kQSlotBytes;
@@ -656,10 +727,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
-    named_bar_sync(1, kConsumerWarps * 32);
+    named_bar_sync(1, kConsumerThreads);
     const bool split = it.nsplit > 1;
 #pragma unroll
-    for (int o = ct; o < G * kHeadDim; o += kConsumerWarps * 32) {
+    for (int o = ct; o < G * kHeadDim; o += kConsumerThreads) {
       const int head = o / kHeadDim, d = o % kHeadDim;
       float M = -INFINITY;
 #pragma unroll
@@ -681,47 +752,49 @@ __global__ void __launch_bounds__(kThreads, 2)
         store_out(a, row * kHeadDim + d, val);
         if (d == 0 && a.lse) a.lse[row] = lse2 * kLn2;
       } else {
-        const size_t prow = (size_t)i * G + head;  // partial slot = item index
+        const size_t prow = (size_t)item_idx * G + head;  // partial slot = item index
         a.part_o[prow * kHeadDim + d] = val;
         if (d == 0) a.part_lse[prow] = lse2;
       }
     }
     if (split) {
-      // ---- a3: the last split of (b, kv head) to finish combines all splits
-      __threadfence();
-      named_bar_sync(1, kConsumerWarps * 32);
+      // ---- a3: the last split of (b, kv head) to finish combines all splits.
+      // Release: bar.sync orders every thread's partial stores before thread 0's
+      // acq_rel ticket (cumulative); acquire: the ticket, then bar.sync, then reads.
+      named_bar_sync(1, kConsumerThreads);
       if (ct == 0) {
         int* ctr = a.counters + (size_t)it.b * a.Hkv + it.h;
-        const int old = atomicAdd(ctr, 1);
+        const int old = atom_add_acq_rel_gpu(ctr, 1);
         const int last = (old == it.nsplit - 1);
         if (last) *ctr = 0;  // self-cleaning: ready for the next run with the same plan
         *s_flag = last;
       }
-      named_bar_sync(1, kConsumerWarps * 32);
+      named_bar_sync(1, kConsumerThreads);
       if (*s_flag) {
-        __threadfence();
         float* s_lse = merge_o;  // reuse the merge area: [nsplit][G] base-2 lse
         const int ns = it.nsplit;
-        for (int x = ct; x < ns * G; x += kConsumerWarps * 32)
+        for (int x = ct; x < ns * G; x += kConsumerThreads)
           s_lse[x] = __ldcg(a.part_lse + (size_t)it.part_base * G + x);
-        named_bar_sync(1, kConsumerWarps * 32);
+        named_bar_sync(1, kConsumerThreads);
 #pragma unroll
-        for (int o = ct; o < G * kHeadDim; o += kConsumerWarps * 32) {
+        for (int o = ct; o < G * kHeadDim; o += kConsumerThreads) {
           const int head = o / kHeadDim, d = o % kHeadDim;
           float M = -INFINITY;
           for (int s = 0; s < ns; ++s) M = fmaxf(M, s_lse[s * G + head]);
           float sum = 0.f, L = 0.f;
           const float* po = a.part_o + ((size_t)it.part_base * G + head) * kHeadDim + d;
           int s = 0;
-          for (; s + 4 <= ns; s += 4) {
-            const float v0 = __ldcg(po + (size_t)(s + 0) * G * kHeadDim);
-            const float v1 = __ldcg(po + (size_t)(s + 1) * G * kHeadDim);
-            const float v2 = __ldcg(po + (size_t)(s + 2) * G * kHeadDim);
-            const float v3 = __ldcg(po + (size_t)(s + 3) * G * kHeadDim);
-            const float w0 = ex2(s_lse[(s + 0) * G + head] - M), w1 = ex2(s_lse[(s + 1) * G + head] - M);
-            const float w2 = ex2(s_lse[(s + 2) * G + head] - M), w3 = ex2(s_lse[(s + 3) * G + head] - M);
-            sum += w0 * v0 + w1 * v1 + w2 * v2 + w3 * v3;
-            L += (w0 + w1) + (w2 + w3);
+          for (; s + 8 <= ns; s += 8) {
+            float v[8], w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(po + (size_t)(s + u) * G * kHeadDim);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) w[u] = ex2(s_lse[(s + u) * G + head] - M);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              sum += w[u] * v[u];
+              L += w[u];
+            }
           }
           for (; s < ns; ++s) {
             const float w = ex2(s_lse[s * G + head] - M);
@@ -734,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
-    named_bar_sync(1, kConsumerWarps * 32);  // merge area free for the next item
+    named_bar_sync(1, kConsumerThreads);  // merge area free for the next item
   }
 }
 
@@ -753,18 +826,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-// Pool [num_pages, Hkv, 16, 128] bf16 viewed as a 2-D tensor of num_pages*Hkv*16
-// rows x 128 columns; box = 16 rows x 64 columns (128 B), 128-byte swizzle.
+// Pool [num_pages, Hkv, 16, 128] bf16 viewed as a 3-D tensor
+// (64 columns, num_pages*Hkv*16 rows of 256 B, 2 column halves 128 B apart);
+// one box = 64 x 16 x 2 = one whole (page, kv head) slice of 4 KB, landing in
+// shared memory as two 16-row x 128-B halves with the 128-byte swizzle.
 l4_status make_tmap(CUtensorMap* tm, const void* base, int64_t rows) {
   auto enc = get_encode_fn();
   if (!enc) return fail(L4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no device)");
   if (rows <= 0 || rows > ((int64_t)1 << 32)) return fail(L4_ERR_INVALID_ARG, "KV pool too large for a tensor map");
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(L4_ERR_INVALID_ARG, "KV pool must be 16-byte aligned");
-  cuuint64_t dims[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kHeadDim * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)kPage};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)kHeadDim * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)kPage, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -788,10 +863,20 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunA
     }
     attr_set[dev] = true;
   }
-  decode_kernel<G><<<grid, kThreads, SmemLayout::alloc, st>>>(tk, tv, a);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SmemLayout::alloc;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: overlap with the planner
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<G>, tk, tv, a);
   if (e != cudaSuccess) {
     set_error("decode_kernel launch failed: %s", cudaGetErrorString(e));
+    cudaGetLastError();
     return L4_ERR_CUDA;
   }
   return L4_OK;
@@ -819,8 +904,7 @@ l4_status device_ctas(int* ctas_out) {
     set_error("l4 requires an sm_100a (B200) device; device %d has compute capability %d.x", dev, major);
     return L4_ERR_CUDA;
   }
-  // Two persistent CTAs per SM (each ~92 KB of shared memory, 160 threads).
-  const int ctas = num_ctas_for(sms, 2);
+  const int ctas = sms * 2;  // two persistent CTAs per SM (~92 KB shared memory, 160 threads each)
   if (dev < 64) cache[dev] = ctas;
   *ctas_out = ctas;
   return L4_OK;
@@ -843,7 +927,6 @@ extern "C" size_t l4_decode_workspace_size(const l4_decode_params* p, int64_t ma
   const int cap = items_cap_for(p, max_total_pages, ctas);
   return ws_layout(p->batch, p->num_kv_heads, G, cap).total;
 }
-
 
 static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, const int32_t* page_indptr,
                            int64_t total_pages, void* workspace, size_t workspace_bytes, cudaStream_t st) {
@@ -874,10 +957,10 @@ static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, con
   a.header = reinterpret_cast<PlanHeader*>(ws + L.header);
   a.items = reinterpret_cast<WorkItem*>(ws + L.items);
   a.counters = reinterpret_cast<int*>(ws + L.counters);
-  const size_t smem = (size_t)2 * std::max(p->batch, 1) * sizeof(int);
+  const size_t smem = (size_t)4 * std::max(p->batch, 1) * sizeof(int);
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxBatch * (int)sizeof(int));
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kMaxBatch * (int)sizeof(int));
   });
   plan_kernel<<<1, kPlanThreads, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
@@ -895,7 +978,8 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   l4_status s = check_params(p, &G);
   if (s != L4_OK) return s;
   if (p->batch == 0) return L4_OK;
-  L4_CHECK_ARG(q && k_pages && v_pages && out && page_indices, "q/k_pages/v_pages/out/page_indices is NULL");
+  // page_indices may be NULL only when every request is empty (indptr[B] == 0).
+  L4_CHECK_ARG(q && k_pages && v_pages && out, "q/k_pages/v_pages/out is NULL");
   L4_CHECK_ARG(num_pages >= 1, "num_pages must be >= 1");
   L4_CHECK_ARG((reinterpret_cast<uintptr_t>(q) & 15) == 0, "q must be 16-byte aligned");
   if (!workspace) return fail(L4_ERR_WORKSPACE, "workspace is NULL");
@@ -918,7 +1002,7 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   a.lse = lse;
   a.indices = page_indices;
   a.items = reinterpret_cast<const WorkItem*>(ws + L.items);
-  a.header = reinterpret_cast<const PlanHeader*>(ws + L.header);
+  a.header = reinterpret_cast<PlanHeader*>(ws + L.header);
   a.counters = reinterpret_cast<int*>(ws + L.counters);
   a.part_o = reinterpret_cast<float*>(ws + L.part_o);
   a.part_lse = reinterpret_cast<float*>(ws + L.part_lse);

@@ -157,10 +157,14 @@ def test_plan_covers_every_token_once():
                 covered[key] = 1
             if pe == base + npg and L > 0:
                 assert last_valid == L - (npg - 1) * 16
-            sizes.append(pe - pb)
+            # length bin of the item = bit_length of its request's largest split
+            sizes.append(0 if npg == 0 else -(-npg // ns))
+            # requests of <= 2C pages are never split
+            if npg <= 2 * info.chunk_pages:
+                assert ns == 1
         expect = sum(8 * ((int(L) + 15) // 16) for L in table.kv_len)
         assert len(covered) == expect
-        # length-binned, longest bin first: bit_length of item size is non-increasing
+        # length-binned, longest bin first: bins are non-increasing along the work list
         bl = [int(x).bit_length() for x in sizes]
         assert all(a >= b for a, b in zip(bl, bl[1:]))
 
