@@ -186,38 +186,59 @@ def time_steps(wl: Workload, steps: int, warmup: int, run_only=False):
 
 
 def time_e2e(wl: Workload, steps: int, warmup: int):
-    """Same metric through the public API with HOST buffers: every step copies q,
-    kv_len, indptr, indices H2D from pinned memory, runs plan+run, copies out D2H."""
+    """Same metric through the public API with HOST buffers.  Every step copies
+    its inputs (q, kv_len, indptr, indices) H2D from pinned memory, runs the
+    plan + split-KV kernels and copies the output D2H.  Copies run on their own
+    streams, double-buffered, so step i+1's H2D and step i-1's D2H overlap step
+    i's kernels (what a serving loop does); the timed region spans the first
+    H2D to the last D2H."""
     import torch
-    l4, params, ws = make_l4(wl)
-    st = torch.cuda.current_stream()
-    h_q = wl.q.cpu().pin_memory()
-    h_kl = wl.kv_len.cpu().pin_memory()
-    h_ip = wl.indptr.cpu().pin_memory()
-    h_ix = wl.indices.cpu().pin_memory()
-    h_out = torch.empty(wl.out.shape, dtype=torch.float32).pin_memory()
-    d_q, d_kl, d_ip, d_ix = (torch.empty_like(wl.q), torch.empty_like(wl.kv_len), torch.empty_like(wl.indptr),
-                             torch.empty_like(wl.indices))
-    h2d = sum(t.numel() * t.element_size() for t in (h_q, h_kl, h_ip, h_ix))
-    d2h = h_out.numel() * h_out.element_size()
+    l4, params, ws0 = make_l4(wl)
+    ws = [ws0, torch.empty_like(ws0)]
+    s_h2d, s_cmp, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    h_in = [wl.q.cpu().pin_memory(), wl.kv_len.cpu().pin_memory(), wl.indptr.cpu().pin_memory(),
+            wl.indices.cpu().pin_memory()]
+    d_in = [[torch.empty_like(t, device="cuda") for t in h_in] for _ in range(2)]
+    d_out = [torch.empty_like(wl.out) for _ in range(2)]
+    d_lse = [torch.empty_like(wl.lse) for _ in range(2)]
+    h_out = [torch.empty(wl.out.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+    h2d = sum(t.numel() * t.element_size() for t in h_in)
+    d2h = h_out[0].numel() * h_out[0].element_size()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_cmp + ev_out:
+        e.record(s_cmp)
 
-    def step():
-        d_q.copy_(h_q, non_blocking=True)
-        d_kl.copy_(h_kl, non_blocking=True)
-        d_ip.copy_(h_ip, non_blocking=True)
-        d_ix.copy_(h_ix, non_blocking=True)
-        l4.decode_plan(params, d_kl, d_ip, wl.table.total_pages, ws)
-        l4.decode_run(params, d_q, wl.k, wl.v, d_ix, wl.out, wl.lse, ws)
-        h_out.copy_(wl.out, non_blocking=True)
+    def step(i):
+        b = i % 2
+        with torch.cuda.stream(s_h2d):
+            s_h2d.wait_event(ev_cmp[b])            # step i-2 finished reading these inputs
+            for d, h in zip(d_in[b], h_in):
+                d.copy_(h, non_blocking=True)
+            ev_in[b].record(s_h2d)
+        with torch.cuda.stream(s_cmp):
+            s_cmp.wait_event(ev_in[b])
+            s_cmp.wait_event(ev_out[b])            # step i-2's output has been copied out
+            q, kl, ip, ix = d_in[b]
+            l4.decode_plan(params, kl, ip, wl.table.total_pages, ws[b], stream=s_cmp)
+            l4.decode_run(params, q, wl.k, wl.v, ix, d_out[b], d_lse[b], ws[b], stream=s_cmp)
+            ev_cmp[b].record(s_cmp)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(ev_cmp[b])
+            h_out[b].copy_(d_out[b], non_blocking=True)
+            ev_out[b].record(s_d2h)
 
-    for _ in range(warmup):
-        step()
+    for i in range(warmup):
+        step(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(steps):
-        step()
-    e1.record(st)
+    e0.record(s_h2d)
+    for i in range(steps):
+        step(i)
+    s_d2h.synchronize()
+    s_h2d.wait_stream(s_d2h)
+    e1.record(s_h2d)
     e1.synchronize()
     return e0.elapsed_time(e1), h2d, d2h
 

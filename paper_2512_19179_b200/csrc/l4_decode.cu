@@ -173,26 +173,30 @@ struct PlanArgs {
   int* counters;
 };
 
-__device__ __forceinline__ int warp_incl_scan(int v) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) >= o) v += t;
-  }
-  return v;
-}
+constexpr int kPlanMaxWarps = kPlanThreads / 32;
 
-// Block-wide exclusive scan of one int per thread (1024 threads).
+// Block-wide exclusive scan of one int per thread; returns the prefix, writes the total.
 __device__ int block_excl_scan(int v, int* total, int* s_warp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = warp_incl_scan(v);
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
   __syncthreads();
   if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    int w = s_warp[lane];
-    int wi = warp_incl_scan(w);
-    s_warp[lane] = wi - w;
+    const int nw = blockDim.x >> 5;
+    const int w = lane < nw ? s_warp[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < nw) s_warp[lane] = wi - w;
     if (lane == 31) s_warp[32] = wi;
   }
   __syncthreads();
@@ -200,33 +204,42 @@ __device__ int block_excl_scan(int v, int* total, int* s_warp) {
   return s_warp[warp] + incl - v;
 }
 
-// Block-wide sum (int64) and max (int) in one pass.
-__device__ void block_sum_max(long long v, int m, long long* s_ll, int* s_i, long long* sum_out, int* max_out) {
+// Block-wide (sum int64, max int, or bits) in one pass.
+__device__ void block_reduce3(long long v, int m, unsigned bits, long long* s_ll, int* s_i, unsigned* s_u,
+                              long long* sum_out, int* max_out, unsigned* or_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     v += __shfl_xor_sync(0xffffffffu, v, o);
     m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    bits |= __shfl_xor_sync(0xffffffffu, bits, o);
   }
   __syncthreads();
   if (lane == 0) {
     s_ll[warp] = v;
     s_i[warp] = m;
+    s_u[warp] = bits;
   }
   __syncthreads();
   long long t = 0;
   int mm = 0;
+  unsigned bb = 0;
+#pragma unroll 8
   for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
     t += s_ll[i];
     mm = max(mm, s_i[i]);
+    bb |= s_u[i];
   }
   *sum_out = t;
   *max_out = mm;
+  *or_out = bb;
 }
 
-__device__ __forceinline__ int nsplit_of(int pages, long long C) {
-  if (pages <= (long long)kNoSplitFactor * C) return 1;  // also pages == 0
-  return (int)((pages + C - 1) / C);
+__device__ __forceinline__ int pages_of(int L) { return L > 0 ? (L + kPage - 1) / kPage : 0; }
+
+__device__ __forceinline__ int nsplit_of(int pages, int C) {
+  if (pages <= kNoSplitFactor * C) return 1;  // also pages == 0
+  return (pages + C - 1) / C;
 }
 
 __device__ __forceinline__ int bin_of(int pages, int nsplit) {
@@ -235,139 +248,161 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
   return min(kNumBins - 1, 32 - __clz(ip));      // bit_length(ip)
 }
 
-constexpr int kPlanMaxR = kMaxBatch / kPlanThreads;  // requests per thread
-
+// One CTA of 1024 threads.  Requests are ordered by length bin, longest bin
+// first, and by request index inside a bin (deterministic plans); each request
+// contributes nsplit * Hkv items, contiguous per (request, kv head).
 __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
   // PDL: let the dependent decode kernel start its prologue now; it waits
   // (griddepcontrol.wait) for this grid's completion before reading the plan.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  extern __shared__ int plan_smem[];  // s_len[B], s_ptr[B], s_off[B], s_b[B]
+  extern __shared__ int plan_smem[];  // s_len[B], s_ptr[B], s_rb[B] (request at rank), s_off[B]
   const int Bs = max(a.B, 1);
   int* s_len = plan_smem;
   int* s_ptr = plan_smem + Bs;
-  int* s_off = plan_smem + 2 * Bs;
-  int* s_b = plan_smem + 3 * Bs;
+  int* s_rb = plan_smem + 2 * Bs;
+  int* s_off = plan_smem + 3 * Bs;
   __shared__ long long s_ll[32];
   __shared__ int s_i[33];
+  __shared__ unsigned s_u[32];
   __shared__ int s_hist[kNumBins];
-  const int tid = threadIdx.x;
-  for (int b = tid; b < a.B; b += kPlanThreads) {
+  __shared__ int s_binbase[kNumBins];
+  __shared__ int s_wb[kPlanMaxWarps][kNumBins];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x, nwarps = nthr >> 5;
+  for (int b = tid; b < a.B; b += nthr) {
     s_len[b] = a.kv_len[b];
     s_ptr[b] = a.indptr[b];
   }
   if (tid < kNumBins) s_hist[tid] = 0;
   __syncthreads();
-  const int R = (a.B + kPlanThreads - 1) / kPlanThreads;
 
-  int pages[kPlanMaxR];
-  long long my_sum = 0;
-  int my_max = 0;
-#pragma unroll
-  for (int r = 0; r < kPlanMaxR; ++r) {
-    const int b = tid * R + r;
-    int pg = 0;
-    if (r < R && b < a.B) {
-      const int L = s_len[b];
-      pg = L > 0 ? (L + kPage - 1) / kPage : 0;
-    }
-    pages[r] = pg;
-    my_sum += pg;
-    my_max = max(my_max, pg);
-  }
   long long T;
   int Pmax;
-  block_sum_max(my_sum, my_max, s_ll, s_i, &T, &Pmax);
-
+  unsigned unused;
+  {
+    long long sum = 0;
+    int mx = 0;
+    for (int b = tid; b < a.B; b += nthr) {
+      const int pg = pages_of(s_len[b]);
+      sum += pg;
+      mx = max(mx, pg);
+    }
+    block_reduce3(sum, mx, 0u, s_ll, s_i, s_u, &T, &Pmax, &unused);
+  }
   // chunk size C (pages per work item)
-  long long C;
+  long long Cl;
   if (a.forced_chunk > 0) {
-    C = a.forced_chunk;
+    Cl = a.forced_chunk;
   } else if (a.forced_chunk < 0) {
-    C = (long long)INT_MAX;
+    Cl = INT_MAX / 4;
   } else {
     const long long denom = (long long)a.num_ctas * kItemsPerCta;
-    C = max((long long)kMinChunk, (T * a.Hkv + denom - 1) / denom);
+    Cl = max((long long)kMinChunk, (T * a.Hkv + denom - 1) / denom);
   }
-  C = max(C, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
+  Cl = max(Cl, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
+  int C = (int)min(Cl, (long long)(INT_MAX / 4));
   long long N;
   for (;;) {  // grow C until the work list fits the workspace (block-uniform loop)
-    long long my_items = 0;
-#pragma unroll
-    for (int r = 0; r < kPlanMaxR; ++r)
-      if (r < R && tid * R + r < a.B) my_items += (long long)nsplit_of(pages[r], C) * a.Hkv;
+    long long items = 0;
+    for (int b = tid; b < a.B; b += nthr) items += (long long)nsplit_of(pages_of(s_len[b]), C) * a.Hkv;
     int dummy;
-    block_sum_max(my_items, 0, s_ll, s_i, &N, &dummy);
-    if (N <= a.items_cap) break;
+    block_reduce3(items, 0, 0u, s_ll, s_i, s_u, &N, &dummy, &unused);
+    if (N <= a.items_cap || C >= INT_MAX / 8) break;
     C *= 2;
   }
 
-  // ---- length bins, longest first (stable by request index within a bin)
-  int bins[kPlanMaxR];
-#pragma unroll
-  for (int r = 0; r < kPlanMaxR; ++r) {
-    const bool valid = r < R && tid * R + r < a.B;
-    bins[r] = valid ? bin_of(pages[r], nsplit_of(pages[r], C)) : -1;
-    if (valid) atomicAdd(&s_hist[bins[r]], 1);
-  }
-  __syncthreads();
-  int base_items = 0, base_rank = 0;
-  for (int bin = kNumBins - 1; bin >= 0; --bin) {
-    if (s_hist[bin] == 0) continue;  // block-uniform
-    int my_cnt = 0, my_n = 0;
-#pragma unroll
-    for (int r = 0; r < kPlanMaxR; ++r)
-      if (bins[r] == bin) {
-        my_cnt += nsplit_of(pages[r], C) * a.Hkv;
-        my_n += 1;
-      }
-    // one scan of (items << 16 | requests) would overflow; do two small scans
-    int tot_items, tot_n;
-    const int ex_items = block_excl_scan(my_cnt, &tot_items, s_i);
-    const int ex_n = block_excl_scan(my_n, &tot_n, s_i);
-    int off = base_items + ex_items, rank = base_rank + ex_n;
-#pragma unroll
-    for (int r = 0; r < kPlanMaxR; ++r)
-      if (bins[r] == bin) {
-        s_off[rank] = off;
-        s_b[rank] = tid * R + r;
-        off += nsplit_of(pages[r], C) * a.Hkv;
-        rank += 1;
-      }
-    base_items += tot_items;
-    base_rank += tot_n;
-  }
-  __syncthreads();
-
-  // ---- write the items cooperatively: item i -> request by binary search over s_off
-  const int nreq = a.B;
-  for (int i = tid; i < (int)N; i += kPlanThreads) {
-    int lo = 0, hi = nreq - 1;
-    while (lo < hi) {  // last rank with s_off[rank] <= i
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+  // ---- ranks: requests per bin, bins in descending order
+  for (int t0 = 0; t0 < a.B; t0 += nthr) {  // warp-aggregated histogram of bins
+    const int b = t0 + tid;
+    int bin = -1;
+    if (b < a.B) {
+      const int pg = pages_of(s_len[b]);
+      bin = bin_of(pg, nsplit_of(pg, C));
     }
-    const int b = s_b[lo];
-    const int L = s_len[b];
-    const int pg = L > 0 ? (L + kPage - 1) / kPage : 0;
-    const int ns = nsplit_of(pg, C);
-    const int local = i - s_off[lo];
-    const int h = local / ns, s = local - h * ns;
-    const int p0 = (int)(((long long)s * pg) / ns);
-    const int p1 = (int)(((long long)(s + 1) * pg) / ns);
-    const int base = s_ptr[b];
-    int4 w0 = make_int4(b, h, base + p0, base + p1);
-    int4 w1 = make_int4((p1 == pg && pg > 0) ? (L - (pg - 1) * kPage) : (p1 > p0 ? kPage : 0),
-                        s_off[lo] + h * ns, ns, s);
-    int4* dst = reinterpret_cast<int4*>(a.items + i);
-    dst[0] = w0;
-    dst[1] = w1;
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[bin], __popc(peers));
   }
-  for (int i = tid; i < a.B * a.Hkv; i += kPlanThreads) a.counters[i] = 0;
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan over bins, highest bin first
+    const int bin = kNumBins - 1 - lane;
+    const int h = s_hist[bin];
+    int incl = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    s_binbase[bin] = incl - h;
+  }
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int tile = 0; tile < a.B; tile += nthr) {  // block-uniform
+    const int b = tile + tid;
+    int bin = -1;
+    if (b < a.B) {
+      const int pg = pages_of(s_len[b]);
+      bin = bin_of(pg, nsplit_of(pg, C));
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    const int lower = __popc(peers & lt_mask);
+    __syncthreads();  // previous tile finished with s_wb / s_binbase
+    for (int x = tid; x < nwarps * kNumBins; x += nthr) (&s_wb[0][0])[x] = 0;
+    __syncthreads();
+    if (bin >= 0 && lower == 0) s_wb[warp][bin] = __popc(peers);
+    __syncthreads();
+    if (tid < kNumBins) {  // per bin: exclusive running count over warps (request order)
+      int run = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const int c = s_wb[w][tid];
+        s_wb[w][tid] = run;
+        run += c;
+      }
+      s_i[tid] = run;  // this tile's requests in bin tid
+    }
+    __syncthreads();
+    if (bin >= 0) s_rb[s_binbase[bin] + s_wb[warp][bin] + lower] = b;
+    __syncthreads();
+    if (tid < kNumBins) s_binbase[tid] += s_i[tid];
+  }
+  __syncthreads();
+  // ---- item offsets: exclusive scan of nsplit * Hkv in rank order
+  {
+    int carry = 0;
+    for (int tile = 0; tile < a.B; tile += nthr) {
+      const int r = tile + tid;
+      int cnt = 0;
+      if (r < a.B) cnt = nsplit_of(pages_of(s_len[s_rb[r]]), C) * a.Hkv;
+      int tot;
+      const int ex = block_excl_scan(cnt, &tot, s_i);
+      if (r < a.B) s_off[r] = carry + ex;
+      carry += tot;
+    }
+  }
+  __syncthreads();
+  // ---- items: one thread per (request rank, kv head) writes that pair's splits
+  for (int x = tid; x < a.B * a.Hkv; x += nthr) {
+    const int r = x / a.Hkv, h = x - r * a.Hkv;
+    const int b = s_rb[r];
+    const int L = s_len[b];
+    const int pg = pages_of(L);
+    const int ns = nsplit_of(pg, C);
+    const int first = s_off[r] + h * ns;
+    const int pbase = s_ptr[b];
+    const int last_valid = pg > 0 ? L - (pg - 1) * kPage : 0;
+    int p0 = 0;
+    for (int sp = 0; sp < ns; ++sp) {
+      const int p1 = ((sp + 1) * pg) / ns;  // pg * ns < 2^31 (ns <= 512)
+      int4* dst = reinterpret_cast<int4*>(a.items + first + sp);
+      dst[0] = make_int4(b, h, pbase + p0, pbase + p1);
+      dst[1] = make_int4(p1 == pg ? last_valid : kPage, first, ns, sp);
+      p0 = p1;
+    }
+  }
+  for (int x = tid; x < a.B * a.Hkv; x += nthr) a.counters[x] = 0;
   if (tid == 0) {
     PlanHeader hd;
     memset(&hd, 0, sizeof(hd));
     hd.n_items = (int)N;
-    hd.chunk = (int)min(C, (long long)INT_MAX);
+    hd.chunk = C;
     hd.num_ctas = a.num_ctas;
     hd.max_splits = nsplit_of(Pmax, C);
     hd.batch = a.B;
@@ -856,6 +891,9 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunA
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemLayout::alloc);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(decode_kernel<G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
       cudaGetLastError();
@@ -961,8 +999,12 @@ static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, con
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kMaxBatch * (int)sizeof(int));
+    // same L1/shared carveout as decode_kernel: no SM reconfiguration between the two launches
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   });
-  plan_kernel<<<1, kPlanThreads, smem, st>>>(a);
+  // one warp per 32 requests (>= 4 warps, <= 32): latency, not throughput, bounds this kernel
+  const int threads = std::min(kPlanThreads, std::max(128, (p->batch + 31) / 32 * 32));
+  plan_kernel<<<1, threads, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("plan_kernel launch failed: %s", cudaGetErrorString(e));

@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+for w in c2 c3 c4; do timeout 300 python scripts/microbench.py --workload $w; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:plan_kernel -s 5 -c 1 \
+  -o gpurun_out/prof_plan_c3 -f python scripts/microbench.py --workload c3 > gpurun_out/prof_plan.log 2>&1
+tail -1 gpurun_out/prof_plan.log

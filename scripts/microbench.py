@@ -1,0 +1,69 @@
+"""Development micro-benchmarks (device time via CUDA events): planner alone,
+run alone, plan+run, for a named workload."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import bench
+from paper_2512_19179_b200 import l4
+
+
+def timeit(fn, iters=50, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / iters * 1e3  # us
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--chunk", type=int, default=0)
+    args = ap.parse_args()
+    spec = bench.WORKLOADS[args.workload]
+    wl = bench.Workload(args.workload, spec["lens"](), spec["shape"])
+    p = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, chunk_pages=args.chunk)
+    ws = l4.alloc_workspace(p, wl.table.total_pages)
+    plan = lambda: l4.decode_plan(p, wl.kv_len, wl.indptr, wl.table.total_pages, ws)
+    run = lambda: l4.decode_run(p, wl.q, wl.k, wl.v, wl.indices, wl.out, wl.lse, ws)
+    both = lambda: (plan(), run())
+    plan()
+    t_plan = timeit(plan)
+    t_run = timeit(run)
+    t_both = timeit(both)
+    # device-only cost: the same calls captured in a CUDA graph (no host launch overhead)
+    def graph_time(fn, reps=20):
+        s = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            fn()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(reps):
+                    fn()
+        return timeit(g.replay, iters=10, warm=2) / reps
+    try:
+        g_plan, g_run, g_both = graph_time(plan), graph_time(run), graph_time(both)
+        print(f"  graph: plan {g_plan:.2f} us, run {g_run:.2f} us, plan+run {g_both:.2f} us "
+              f"({wl.bytes_kv / (g_both * 1e-6) / 1e9:.0f} GB/s)")
+    except Exception as e:  # noqa
+        print("  graph capture failed:", e)
+    info = l4.plan_info(ws)
+    gbs = wl.bytes_kv / (t_both * 1e-6) / 1e9
+    print(f"{args.workload}: plan {t_plan:.2f} us, run {t_run:.2f} us ({wl.bytes_kv / (t_run * 1e-6) / 1e9:.0f} GB/s), "
+          f"plan+run {t_both:.2f} us ({gbs:.0f} GB/s); items {info.num_items} chunk {info.chunk_pages}")
+
+
+if __name__ == "__main__":
+    main()
