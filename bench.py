@@ -317,6 +317,139 @@ def mixed_vs_binned(steps: int, warmup: int):
     return res
 
 
+# ----------------------------------------------------------------------------- pipeline (N > 1)
+def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, seed=0, shape=None):
+    """C5: the length-aware pipeline on `world` GPUs.  Every step each rank runs the hot path
+    (plan + split-KV kernel) on its resident batch, then the replicated control plane advances
+    (tokens appended, handovers, retirements, arrivals) and KV pages of handed-over requests
+    move between ranks (l4_pack_pages -> NCCL send/recv -> l4_unpack_pages).
+    Returns per-rank totals (device time measured with CUDA events on the compute stream)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_19179_b200 import l4, pipeline
+    shape = shape or synth.SHAPE_LLAMA3_8B
+    sim = pipeline.ClusterSim(stages, concurrency=world * per_rank, seed=seed)
+    budget_pages = sim.token_budget // 16 * 5 // 4 + 2 * sim.batch_cap
+    rt = pipeline.RankRuntime(sim, rank, budget_pages, shape, pipeline.DeviceOps(shape, device, seed + rank))
+    cap = sim.batch_cap
+    g = torch.Generator(device=device).manual_seed(seed + 100 + rank)
+    q = torch.randn(cap, shape.num_q_heads, 128, device=device, generator=g).to(torch.bfloat16)
+    out = torch.empty(cap, shape.num_q_heads, 128, dtype=torch.float32, device=device)
+    lse = torch.empty(cap, shape.num_q_heads, dtype=torch.float32, device=device)
+    p_max = l4.make_params(cap, shape.num_q_heads, shape.num_kv_heads)
+    ws = l4.alloc_workspace(p_max, budget_pages)
+    pool = rt.pool
+    tot = dict(kv_bytes=0, tokens=0, steps=0, mig_bytes=0, mig_count=0, busy_ms=0.0, req_steps=0, lat_ms_x_req=0.0)
+    evs = []
+    st = torch.cuda.current_stream()
+    t_start = t_end = None
+    for it in range(warmup + steps):
+        timed = it >= warmup
+        if it == warmup:
+            torch.cuda.synchronize()
+            dist.barrier()
+            t_start = torch.cuda.Event(enable_timing=True)
+            t_start.record(st)
+        kv_len, indptr, indices = rt.tables()
+        B = int(kv_len.shape[0])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        if B > 0:
+            d_len = torch.from_numpy(kv_len).to(device, non_blocking=True)
+            d_ptr = torch.from_numpy(indptr).to(device, non_blocking=True)
+            d_idx = torch.from_numpy(indices).to(device, non_blocking=True)
+            params = l4.make_params(B, shape.num_q_heads, shape.num_kv_heads)
+            l4.decode_plan(params, d_len, d_ptr, int(indices.shape[0]), ws)
+            l4.decode_run(params, q[:B], pool["k"], pool["v"], d_idx, out[:B], lse[:B], ws)
+        e1.record(st)
+        ev = sim.step()
+        before = rt.stats["migrated_bytes"]
+        rt.apply(ev, dist)
+        if timed:
+            evs.append((e0, e1, B))
+            tot["kv_bytes"] += int(4 * shape.num_kv_heads * 128 * int(kv_len.sum()))
+            tot["tokens"] += B
+            tot["steps"] += 1
+            tot["mig_bytes"] += rt.stats["migrated_bytes"] - before
+            tot["mig_count"] += sum(1 for m in ev.migrations if m[1] == rank)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_end.record(st)
+    torch.cuda.synchronize()
+    for e0, e1, B in evs:
+        dt = e0.elapsed_time(e1)
+        tot["busy_ms"] += dt
+        tot["lat_ms_x_req"] += dt * B
+        tot["req_steps"] += B
+    tot["elapsed_ms"] = t_start.elapsed_time(t_end)
+    tot["fingerprint"] = sim.fingerprint()
+    tot["stages"] = stages
+    return tot
+
+
+def pipeline_line(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2512_19179_b200 import pipeline
+    device = torch.device("cuda", local)
+    peak, peak_src = load_peaks()
+    stages, obj = pipeline.plan_stages(world, seed=0)
+    rr = [(0, stages[-1][1], world)]                       # length-agnostic: one stage of all instances
+    res = {}
+    dist.barrier()                                          # first collective on the group
+    # warm up the NCCL P2P connections between adjacent stages outside the timed region
+    rank_stage = pipeline.assign_ranks(stages)
+    ops = []
+    for s_ in range(world):
+        for d_ in range(world):
+            if rank_stage[d_] == rank_stage[s_] + 1:
+                if rank == s_:
+                    ops.append(dist.P2POp(dist.isend, torch.ones(1, device=device), d_))
+                if rank == d_:
+                    ops.append(dist.P2POp(dist.irecv, torch.empty(1, device=device), s_))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    torch.cuda.synchronize()
+    dist.barrier()
+    for name, st in (("l4", stages), ("round_robin", rr)):
+        t = run_pipeline_arm(st, args.steps, args.warmup, rank, world, device)
+        vec = torch.tensor([t["kv_bytes"], t["tokens"], t["mig_bytes"], t["mig_count"], t["req_steps"],
+                            t["lat_ms_x_req"]], dtype=torch.float64, device=device)
+        dist.all_reduce(vec, op=dist.ReduceOp.SUM)
+        tm = torch.tensor([t["elapsed_ms"], t["busy_ms"]], dtype=torch.float64, device=device)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        fp = torch.tensor([t["fingerprint"] & 0x7FFFFFFF], dtype=torch.int64, device=device)
+        fps = [torch.zeros_like(fp) for _ in range(world)]
+        dist.all_gather(fps, fp)
+        assert all(int(x) == int(fp) for x in fps), "replicated control plane diverged"
+        elapsed = float(tm[0])
+        res[name] = dict(kv_gbs=float(vec[0]) / (elapsed / 1e3) / 1e9, tokens_per_s=float(vec[1]) / (elapsed / 1e3),
+                         elapsed_ms=elapsed, max_busy_ms=float(tm[1]), migrated_bytes=int(vec[2]),
+                         migrations=int(vec[3]), mean_step_latency_ms=float(vec[5]) / max(1.0, float(vec[4])),
+                         stages=[list(x) for x in st])
+    if rank != 0:
+        return None
+    l4r = res["l4"]
+    mig_gbs = None
+    line = {
+        "metric": METRIC, "value": round(l4r["kv_gbs"], 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(l4r["elapsed_ms"] / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "c5-pipeline", "desc": "BASELINE configs[4]: length-aware pipeline, "
+                   f"{world} instances (1 GPU each), Llama-3-8B attention shape, ShareGPT-like closed loop, "
+                   f"{256} resident requests per instance, 1.2M-token KV budget per instance",
+                   "stages": l4r["stages"], "partition_objective": obj,
+                   "parallelism": f"length-aware pipeline over {world} GPUs (l4_partition); KV migration over NCCL P2P",
+                   "l2": "inputs larger than L2; no flush"},
+        "tokens_per_s": round(l4r["tokens_per_s"], 1),
+        "pct_hbm_peak": round(100.0 * l4r["kv_gbs"] / (world * peak), 2),
+        "pipeline": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                     for k, v in res.items()},
+        "gpu_launches": None,
+    }
+    return line
+
+
 # ----------------------------------------------------------------------------- main
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -360,6 +493,8 @@ def main():
     ap.add_argument("--impl", default="l4", choices=["l4", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip mixed-vs-binned / C4 sub-measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of the pipeline")
+    ap.add_argument("--pipeline", action="store_true", help="run the C5 pipeline harness even at N = 1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -372,6 +507,21 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if (ws > 1 and not args.replicas) or args.pipeline:
+        if ws == 1:
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            torch.distributed.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                                 world_size=1, device_id=torch.device("cuda", local))
+        line = pipeline_line(args, ws, rank, local)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+        return 0
     peak, peak_src = load_peaks()
     spec = WORKLOADS[args.workload]
     wl = Workload(args.workload, spec["lens"](), spec["shape"], seed=rank)

@@ -1,0 +1,359 @@
+"""L4 length-aware pipeline over GPUs — host control plane.
+
+  P:255  instances are grouped into length-specialised stages forming a logical pipeline
+  P:267  "when a request arrives, it is routed to the earliest stage whose serving range
+         covers its initial length ... As the sequence grows, if its length exceeds the
+         instance's range, it is migrated to the next stage"
+  P:281  the Coordinator "allocates memory on the target instance, and transfers the KV cache"
+  P:428  KV goes "directly into idle slots"; migration is skipped if no idle cache is
+         available; at most three transfers in flight (excess requests keep running on
+         the source)
+
+Each GPU (rank) is one instance.  ``l4_partition`` (the §4.2 DP, host C++) turns a
+request-length sample into stages; stage k gets the next ``instances_k`` ranks.
+
+The control plane here is REPLICATED and deterministic: every rank simulates the whole
+cluster's request state (ClusterSim) from the same seed, so every rank knows every
+routing / handover / retirement decision without exchanging control messages.  The only
+cross-GPU traffic is KV-page migration (north star).  The data path of each step — the
+decode attention over the local batch and the page pack/unpack — runs in libl4 kernels;
+the transport is torch.distributed send/recv (NCCL over NVLink on GPUs).
+
+Within a stage the receiving rank is the least-loaded one by resident tokens (a simple
+stand-in for the bid-ask protocol, which is a next step).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Tuple
+
+import numpy as np
+
+PAGE = 16
+
+
+@dataclass
+class Req:
+    rid: int
+    I: int
+    O: int
+    L: int          # current length (tokens whose KV is cached)
+    rank: int
+
+
+@dataclass
+class StepEvents:
+    """What happened in one decode step, identical on every rank."""
+    migrations: List[Tuple[int, int, int, int]] = field(default_factory=list)  # (rid, src, dst, L at handover)
+    retired: List[Tuple[int, int]] = field(default_factory=list)               # (rid, rank)
+    admitted: List[Tuple[int, int, int]] = field(default_factory=list)         # (rid, rank, L)
+    deferred: int = 0                                                           # handovers over the cap
+
+
+def assign_ranks(stages) -> List[int]:
+    """rank -> stage index: stage k takes the next instances_k ranks (NVSwitch: placement is free)."""
+    out = []
+    for k, (_, _, m) in enumerate(stages):
+        out.extend([k] * m)
+    return out
+
+
+class RequestStream:
+    """Deterministic (I, O) source shaped like the paper's ShareGPT traces (synth M5)."""
+
+    def __init__(self, seed: int, max_len: int = 131072, chunk: int = 4096):
+        import synth
+        self._synth = synth
+        self.seed, self.max_len, self.chunk = seed, max_len, chunk
+        self._buf: list = []
+        self._k = 0
+        self.next_rid = 0
+
+    def next(self):
+        if not self._buf:
+            I, O = self._synth.requests_sharegpt_like(seed=self.seed * 1000003 + self._k, n=self.chunk,
+                                                      max_len=self.max_len)
+            self._k += 1
+            self._buf = list(zip(I.tolist(), O.tolist()))[::-1]
+        I, O = self._buf.pop()
+        rid = self.next_rid
+        self.next_rid += 1
+        return rid, int(I), int(O)
+
+
+class ClusterSim:
+    """Replicated, deterministic simulation of the cluster's requests (no GPU state).
+
+    Requests live in slots (numpy arrays); every operation is a deterministic function of
+    the seed, so all ranks compute identical states and events.  Per-step work is
+    vectorised; only the few handovers / arrivals run Python loops."""
+
+    def __init__(self, stages, concurrency: int, seed: int = 0, token_budget: int = 1_200_000,
+                 batch_cap: int = 1024, max_transfers: int = 3):
+        self.stages = [(int(lo), int(hi), int(m)) for lo, hi, m in stages]
+        self.rank_stage = np.array(assign_ranks(self.stages), dtype=np.int64)
+        self.n_ranks = len(self.rank_stage)
+        self.stage_hi = np.array([hi for _, hi, _ in self.stages], dtype=np.int64)
+        self.last_stage = len(self.stages) - 1
+        self.stage_ranks = [[r for r in range(self.n_ranks) if self.rank_stage[r] == k] for k in range(len(self.stages))]
+        self.token_budget = token_budget      # admission limit per instance (KV memory)
+        self.batch_cap = batch_cap
+        self.max_transfers = max_transfers
+        self.stream = RequestStream(seed)
+        self.rng = np.random.default_rng(seed + 17)
+        cap = max(16, 2 * concurrency + self.n_ranks * 4)
+        self.rid = np.full(cap, -1, dtype=np.int64)
+        self.I = np.zeros(cap, dtype=np.int64)
+        self.O = np.zeros(cap, dtype=np.int64)
+        self.L = np.zeros(cap, dtype=np.int64)
+        self.rank = np.full(cap, -1, dtype=np.int64)
+        self.active = np.zeros(cap, dtype=bool)
+        self.tokens = np.zeros(self.n_ranks, dtype=np.int64)
+        self.count = np.zeros(self.n_ranks, dtype=np.int64)
+        self.queue: List[Tuple[int, int, int]] = []
+        for _ in range(concurrency):          # stationary start: a random point of each lifetime
+            rid, I, O = self.stream.next()
+            L = I + int(self.rng.integers(0, O))
+            self._place(rid, I, O, L, initial=True)
+
+    @property
+    def reqs(self):
+        """rid -> Req view (diagnostics / tests)."""
+        idx = np.nonzero(self.active)[0]
+        return {int(self.rid[i]): Req(int(self.rid[i]), int(self.I[i]), int(self.O[i]), int(self.L[i]),
+                                      int(self.rank[i])) for i in idx}
+
+    # ---------------------------------------------------------------- routing
+    def stage_of(self, L: int) -> int:
+        """Earliest stage whose range covers length L; the last stage takes the rest."""
+        for k, (lo, hi, _) in enumerate(self.stages):
+            if lo <= L < hi:
+                return k
+        return self.last_stage
+
+    def least_loaded(self, stage: int, extra_tokens: int = 0):
+        best = None
+        for r in self.stage_ranks[stage]:
+            if self.count[r] >= self.batch_cap or self.tokens[r] + extra_tokens > self.token_budget:
+                continue
+            if best is None or self.tokens[r] < self.tokens[best]:
+                best = r
+        return best
+
+    def _free_slot(self):
+        free = np.nonzero(~self.active)[0]
+        if free.size == 0:
+            n = self.rid.size
+            for name in ("rid", "I", "O", "L", "rank"):
+                arr = getattr(self, name)
+                fill = -1 if name in ("rid", "rank") else 0
+                setattr(self, name, np.concatenate([arr, np.full(n, fill, dtype=arr.dtype)]))
+            self.active = np.concatenate([self.active, np.zeros(n, dtype=bool)])
+            return n
+        return int(free[0])
+
+    def _place(self, rid, I, O, L, initial=False):
+        r = self.least_loaded(self.stage_of(L), L + 1)
+        if r is None:
+            if not initial:
+                self.queue.append((rid, I, O))
+            return None
+        i = self._free_slot()
+        self.rid[i], self.I[i], self.O[i], self.L[i], self.rank[i], self.active[i] = rid, I, O, L, r, True
+        self.tokens[r] += L
+        self.count[r] += 1
+        return r
+
+    # ---------------------------------------------------------------- one decode step
+    def step(self) -> StepEvents:
+        ev = StepEvents()
+        act = self.active
+        # 1. every resident request generated one token: its KV grows by one
+        self.L[act] += 1
+        self.tokens += np.bincount(self.rank[act], minlength=self.n_ranks)
+        # 2. retire finished requests (closed loop: each is replaced by an arrival)
+        done = np.nonzero(act & (self.L >= self.I + self.O))[0]
+        for i in done:
+            r = int(self.rank[i])
+            ev.retired.append((int(self.rid[i]), r))
+            self.tokens[r] -= self.L[i]
+            self.count[r] -= 1
+            self.active[i] = False
+        # 3. handover to the next stage when the length leaves the stage range
+        act = self.active
+        st = self.rank_stage[np.maximum(self.rank, 0)]
+        cand = np.nonzero(act & (st != self.last_stage) & (self.L >= self.stage_hi[st]))[0]
+        sent = np.zeros(self.n_ranks, dtype=np.int64)
+        for i in cand:                       # slot order: deterministic on every rank
+            src, L = int(self.rank[i]), int(self.L[i])
+            if sent[src] >= self.max_transfers:        # keep running on the source
+                ev.deferred += 1
+                continue
+            dst = self.least_loaded(self.stage_of(L), L)
+            if dst is None:                            # no idle cache downstream: skip
+                ev.deferred += 1
+                continue
+            self.tokens[src] -= L
+            self.count[src] -= 1
+            self.rank[i] = dst
+            self.tokens[dst] += L
+            self.count[dst] += 1
+            ev.migrations.append((int(self.rid[i]), src, dst, L))
+            sent[src] += 1
+        # 4. arrivals: queued first, then one new request per retirement
+        pending, self.queue = self.queue, []
+        for _ in range(len(done)):
+            pending.append(self.stream.next())
+        for rid, I, O in pending:
+            r = self._place(rid, I, O, I)
+            if r is not None:
+                ev.admitted.append((rid, r, I))
+        return ev
+
+    def batch(self, rank: int):
+        """Resident requests of a rank in slot order: (rid array, L array)."""
+        idx = np.nonzero(self.active & (self.rank == rank))[0]
+        return self.rid[idx], self.L[idx]
+
+    def fingerprint(self) -> int:
+        idx = np.nonzero(self.active)[0]
+        order = np.argsort(self.rid[idx])
+        data = np.stack([self.rid[idx][order], self.L[idx][order], self.rank[idx][order]]).astype(np.int64)
+        h = 1469598103934665603
+        for x in data.ravel().tolist():
+            h = ((h ^ (x & 0xFFFFFFFF)) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+        return h
+
+
+def plan_stages(n_instances: int, seed: int = 0, n_sample: int = 10000, qoe_d=None,
+                bandwidth_Bps: float = 7.7e11, kv_bytes_per_token: int = 131072, mode: int = 0):
+    """l4_partition over a request sample (the period's statistics)."""
+    import synth
+    from . import l4
+    I, O = synth.requests_sharegpt_like(seed=seed, n=n_sample)
+    D = synth.roofline_qoe_d() if qoe_d is None else qoe_d
+    stages, obj = l4.partition(I, O, n_instances, D, bandwidth_Bps, kv_bytes_per_token, mode=mode)
+    return stages, obj
+
+
+class RankRuntime:
+    """One rank's device state: a paged KV pool (one layer materialised), the page tables of
+    its resident requests, and the per-step data path (attention + migration transport).
+
+    ``ops`` provides the device operations; the default is libl4 on CUDA (see DeviceOps).
+    """
+
+    def __init__(self, sim: ClusterSim, rank: int, num_pages: int, shape, ops, seed: int = 0):
+        self.sim, self.rank, self.shape, self.ops = sim, rank, shape, ops
+        self.num_pages = num_pages
+        self.pool = ops.make_pool(num_pages)
+        self.pages: Dict[int, List[int]] = {}
+        rids, Ls = sim.batch(rank)
+        for rid, L in zip(rids.tolist(), Ls.tolist()):
+            self.pages[rid] = ops.alloc(self.pool, -(-L // PAGE))
+        self.stats = dict(migrated_pages=0, migrated_bytes=0, migrations_in=0, migrations_out=0)
+
+    def tables(self):
+        rids, Ls = self.sim.batch(self.rank)
+        kv_len = Ls.astype(np.int32)
+        lists = [self.pages[rid] for rid in rids.tolist()]
+        counts = np.fromiter((len(x) for x in lists), dtype=np.int64, count=len(lists))
+        indptr = np.zeros(len(lists) + 1, dtype=np.int32)
+        indptr[1:] = np.cumsum(counts)
+        indices = (np.fromiter((p for x in lists for p in x), dtype=np.int32, count=int(indptr[-1]))
+                   if lists else np.zeros(0, dtype=np.int32))
+        return kv_len, indptr, indices
+
+    def apply(self, ev: StepEvents, comm):
+        """Apply one step's events to this rank: grow page lists (new tokens), retire,
+        migrate KV pages out/in (P2P), admit new requests."""
+        me = self.rank
+        for rid, r in ev.retired:
+            if r == me and rid in self.pages:
+                self.ops.free(self.pool, self.pages.pop(rid))
+        # growth: the step's new token opens a new page when L-1 is a multiple of 16
+        sim = self.sim
+        mig_out = {m[0] for m in ev.migrations if m[1] == me}
+        grow = np.nonzero(sim.active & ((sim.L - 1) % PAGE == 0))[0]
+        for i in grow:
+            rid = int(sim.rid[i])
+            if rid in self.pages and (int(sim.rank[i]) == me or rid in mig_out):
+                need = -(-int(sim.L[i]) // PAGE)
+                if need > len(self.pages[rid]):
+                    self.pages[rid].extend(self.ops.alloc(self.pool, need - len(self.pages[rid])))
+        sends, recvs = [], []
+        for rid, src, dst, L in ev.migrations:
+            if src == me:
+                pages = self.pages.pop(rid)
+                need = -(-L // PAGE)
+                if need > len(pages):
+                    pages = pages + self.ops.alloc(self.pool, need - len(pages))
+                sends.append((rid, dst, pages))
+            elif dst == me:
+                recvs.append((rid, src, -(-L // PAGE)))
+        nbytes = self.ops.transfer(self.pool, sends, recvs, comm, self.pages)
+        for rid, dst, pages in sends:
+            self.ops.free(self.pool, pages)
+            self.stats["migrations_out"] += 1
+            self.stats["migrated_pages"] += len(pages)
+        self.stats["migrations_in"] += len(recvs)
+        self.stats["migrated_bytes"] += nbytes
+        for rid, r, L in ev.admitted:
+            if r == me:
+                self.pages[rid] = self.ops.alloc(self.pool, -(-L // PAGE))   # prefill not emulated
+
+
+class DeviceOps:
+    """libl4 on CUDA: page pool (host allocator over a device KV pool), attention, and the
+    KV-page transport (l4_pack_pages -> NCCL send/recv -> l4_unpack_pages)."""
+
+    def __init__(self, shape, device, seed=0):
+        import torch
+        from . import l4
+        self.torch, self.l4, self.shape, self.device = torch, l4, shape, device
+        self.seed = seed
+
+    def make_pool(self, num_pages):
+        torch = self.torch
+        s = self.shape
+        g = torch.Generator(device=self.device).manual_seed(self.seed)
+        k = torch.empty(num_pages, s.num_kv_heads, PAGE, s.head_dim, dtype=torch.bfloat16, device=self.device)
+        v = torch.empty_like(k)
+        for x in (k, v):
+            for a in range(0, num_pages, 8192):
+                e = min(num_pages, a + 8192)
+                x[a:e] = torch.randn(e - a, *x.shape[1:], device=self.device, generator=g).to(torch.bfloat16)
+        return dict(k=k, v=v, alloc=self.l4.PagePool(num_pages), view=self.l4.kv_view(k, v))
+
+    def alloc(self, pool, n):
+        return pool["alloc"].alloc(n).tolist()
+
+    def free(self, pool, pages):
+        pool["alloc"].free(pages)
+
+    def transfer(self, pool, sends, recvs, comm, page_map):
+        """Pack outgoing pages, exchange with batched NCCL P2P, unpack into newly allocated
+        idle pages.  Returns bytes moved by this rank (sent + received)."""
+        torch, l4, dist = self.torch, self.l4, comm
+        if not sends and not recvs:
+            return 0
+        pb = pool["view"].page_bytes
+        ops, bufs, nbytes = [], [], 0
+        for rid, dst, pages in sends:
+            st = torch.empty(len(pages) * 2 * pb, dtype=torch.uint8, device=self.device)
+            l4.pack_pages(pool["view"], pages, st)
+            ops.append(dist.P2POp(dist.isend, st, dst))
+            nbytes += st.numel()
+        for rid, src, npages in recvs:
+            st = torch.empty(npages * 2 * pb, dtype=torch.uint8, device=self.device)
+            ops.append(dist.P2POp(dist.irecv, st, src))
+            bufs.append((rid, npages, st))
+            nbytes += st.numel()
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        for rid, npages, st in bufs:
+            pages = self.alloc(pool, npages)
+            l4.unpack_pages(pool["view"], pages, st)
+            page_map[rid] = pages
+        return nbytes
