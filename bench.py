@@ -350,17 +350,16 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
             dist.barrier()
             t_start = torch.cuda.Event(enable_timing=True)
             t_start.record(st)
-        kv_len, indptr, indices = rt.tables()
+        kv_len, indptr = rt.device_batch()
         B = int(kv_len.shape[0])
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         if B > 0:
-            d_len = torch.from_numpy(kv_len).to(device, non_blocking=True)
-            d_ptr = torch.from_numpy(indptr).to(device, non_blocking=True)
-            d_idx = torch.from_numpy(indices).to(device, non_blocking=True)
+            d_len = torch.from_numpy(kv_len).pin_memory().to(device, non_blocking=True)
+            d_ptr = torch.from_numpy(indptr).pin_memory().to(device, non_blocking=True)
             params = l4.make_params(B, shape.num_q_heads, shape.num_kv_heads)
-            l4.decode_plan(params, d_len, d_ptr, int(indices.shape[0]), ws)
-            l4.decode_run(params, q[:B], pool["k"], pool["v"], d_idx, out[:B], lse[:B], ws)
+            l4.decode_plan(params, d_len, d_ptr, int(rt.table.numel()), ws)
+            l4.decode_run(params, q[:B], pool["k"], pool["v"], rt.table, out[:B], lse[:B], ws)
         e1.record(st)
         ev = sim.step()
         before = rt.stats["migrated_bytes"]
@@ -368,6 +367,7 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
         if timed:
             evs.append((e0, e1, B))
             tot["kv_bytes"] += int(4 * shape.num_kv_heads * 128 * int(kv_len.sum()))
+            tot["launches"] = tot.get("launches", 0) + (2 if B > 0 else 0)
             tot["tokens"] += B
             tot["steps"] += 1
             tot["mig_bytes"] += rt.stats["migrated_bytes"] - before
@@ -381,6 +381,7 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
         tot["lat_ms_x_req"] += dt * B
         tot["req_steps"] += B
     tot["elapsed_ms"] = t_start.elapsed_time(t_end)
+    tot["launches"] = tot.get("launches", 0) + rt.stats["launches"]
     tot["fingerprint"] = sim.fingerprint()
     tot["stages"] = stages
     return tot
@@ -414,7 +415,7 @@ def pipeline_line(args, world, rank, local):
     for name, st in (("l4", stages), ("round_robin", rr)):
         t = run_pipeline_arm(st, args.steps, args.warmup, rank, world, device)
         vec = torch.tensor([t["kv_bytes"], t["tokens"], t["mig_bytes"], t["mig_count"], t["req_steps"],
-                            t["lat_ms_x_req"]], dtype=torch.float64, device=device)
+                            t["lat_ms_x_req"], t["launches"]], dtype=torch.float64, device=device)
         dist.all_reduce(vec, op=dist.ReduceOp.SUM)
         tm = torch.tensor([t["elapsed_ms"], t["busy_ms"]], dtype=torch.float64, device=device)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -426,6 +427,7 @@ def pipeline_line(args, world, rank, local):
         res[name] = dict(kv_gbs=float(vec[0]) / (elapsed / 1e3) / 1e9, tokens_per_s=float(vec[1]) / (elapsed / 1e3),
                          elapsed_ms=elapsed, max_busy_ms=float(tm[1]), migrated_bytes=int(vec[2]),
                          migrations=int(vec[3]), mean_step_latency_ms=float(vec[5]) / max(1.0, float(vec[4])),
+                         launches=int(vec[6]),
                          stages=[list(x) for x in st])
     if rank != 0:
         return None
@@ -445,7 +447,7 @@ def pipeline_line(args, world, rank, local):
         "pct_hbm_peak": round(100.0 * l4r["kv_gbs"] / (world * peak), 2),
         "pipeline": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                      for k, v in res.items()},
-        "gpu_launches": None,
+        "gpu_launches": int(l4r["launches"]),
     }
     return line
 

@@ -241,20 +241,66 @@ class RankRuntime:
     """One rank's device state: a paged KV pool (one layer materialised), the page tables of
     its resident requests, and the per-step data path (attention + migration transport).
 
-    ``ops`` provides the device operations; the default is libl4 on CUDA (see DeviceOps).
+    Page tables live on the device as a block table [slots, max_pages] (row = one resident
+    request, fixed stride), so the decode kernel gets indptr[b] = slot_b * max_pages and no
+    CSR is rebuilt per step; the host sends only the per-step page-id deltas.
+    ``ops`` provides the device operations (DeviceOps: libl4 on CUDA).
     """
 
-    def __init__(self, sim: ClusterSim, rank: int, num_pages: int, shape, ops, seed: int = 0):
+    def __init__(self, sim: ClusterSim, rank: int, num_pages: int, shape, ops, seed: int = 0,
+                 max_pages_per_req: int = 131072 // PAGE):
         self.sim, self.rank, self.shape, self.ops = sim, rank, shape, ops
         self.num_pages = num_pages
         self.pool = ops.make_pool(num_pages)
+        self.max_pages = max_pages_per_req
+        self.slots_cap = sim.batch_cap
+        self.table = ops.make_table(self.slots_cap, self.max_pages) if hasattr(ops, "make_table") else None
+        self.free_slots = list(range(self.slots_cap))[::-1]
+        self.slot_of: Dict[int, int] = {}
         self.pages: Dict[int, List[int]] = {}
+        self._dpos: List[np.ndarray] = []
+        self._dval: List[np.ndarray] = []
         rids, Ls = sim.batch(rank)
         for rid, L in zip(rids.tolist(), Ls.tolist()):
-            self.pages[rid] = ops.alloc(self.pool, -(-L // PAGE))
-        self.stats = dict(migrated_pages=0, migrated_bytes=0, migrations_in=0, migrations_out=0)
+            self._add(rid, ops.alloc(self.pool, -(-L // PAGE)))
+        self.stats = dict(migrated_pages=0, migrated_bytes=0, migrations_in=0, migrations_out=0, launches=0)
+
+    # ------------------------------------------------------------ page-table bookkeeping
+    def _delta(self, slot, start, pages):
+        if pages:
+            self._dpos.append(slot * self.max_pages + start + np.arange(len(pages), dtype=np.int64))
+            self._dval.append(np.asarray(pages, dtype=np.int32))
+
+    def _add(self, rid, pages):
+        slot = self.free_slots.pop()
+        self.slot_of[rid] = slot
+        self.pages[rid] = list(pages)
+        self._delta(slot, 0, self.pages[rid])
+
+    def _append(self, rid, new_pages):
+        start = len(self.pages[rid])
+        self.pages[rid].extend(new_pages)
+        self._delta(self.slot_of[rid], start, new_pages)
+
+    def _drop(self, rid):
+        self.free_slots.append(self.slot_of.pop(rid))
+        return self.pages.pop(rid)
+
+    def device_batch(self):
+        """(kv_len int32 [B], indptr int32 [B+1]) of the resident batch in slot-table form,
+        after flushing this step's page-table deltas to the device table."""
+        if self._dpos:
+            self.ops.table_update(self.table, np.concatenate(self._dpos), np.concatenate(self._dval))
+            self._dpos, self._dval = [], []
+        rids, Ls = self.sim.batch(self.rank)
+        slots = np.fromiter((self.slot_of[r] for r in rids.tolist()), dtype=np.int64, count=len(rids))
+        indptr = np.empty(len(rids) + 1, dtype=np.int32)
+        indptr[:-1] = slots * self.max_pages
+        indptr[-1] = self.slots_cap * self.max_pages
+        return Ls.astype(np.int32), indptr
 
     def tables(self):
+        """Compact host CSR of the resident batch (tests / diagnostics)."""
         rids, Ls = self.sim.batch(self.rank)
         kv_len = Ls.astype(np.int32)
         lists = [self.pages[rid] for rid in rids.tolist()]
@@ -266,12 +312,12 @@ class RankRuntime:
         return kv_len, indptr, indices
 
     def apply(self, ev: StepEvents, comm):
-        """Apply one step's events to this rank: grow page lists (new tokens), retire,
+        """Apply one step's events to this rank: retire, grow page lists (new tokens),
         migrate KV pages out/in (P2P), admit new requests."""
         me = self.rank
         for rid, r in ev.retired:
             if r == me and rid in self.pages:
-                self.ops.free(self.pool, self.pages.pop(rid))
+                self.ops.free(self.pool, self._drop(rid))
         # growth: the step's new token opens a new page when L-1 is a multiple of 16
         sim = self.sim
         mig_out = {m[0] for m in ev.migrations if m[1] == me}
@@ -281,27 +327,31 @@ class RankRuntime:
             if rid in self.pages and (int(sim.rank[i]) == me or rid in mig_out):
                 need = -(-int(sim.L[i]) // PAGE)
                 if need > len(self.pages[rid]):
-                    self.pages[rid].extend(self.ops.alloc(self.pool, need - len(self.pages[rid])))
+                    self._append(rid, self.ops.alloc(self.pool, need - len(self.pages[rid])))
         sends, recvs = [], []
         for rid, src, dst, L in ev.migrations:
             if src == me:
-                pages = self.pages.pop(rid)
+                pages = self._drop(rid)
                 need = -(-L // PAGE)
                 if need > len(pages):
                     pages = pages + self.ops.alloc(self.pool, need - len(pages))
                 sends.append((rid, dst, pages))
             elif dst == me:
                 recvs.append((rid, src, -(-L // PAGE)))
-        nbytes = self.ops.transfer(self.pool, sends, recvs, comm, self.pages)
+        received: Dict[int, List[int]] = {}
+        nbytes = self.ops.transfer(self.pool, sends, recvs, comm, received)
+        for rid, pages in received.items():
+            self._add(rid, pages)
         for rid, dst, pages in sends:
             self.ops.free(self.pool, pages)
             self.stats["migrations_out"] += 1
             self.stats["migrated_pages"] += len(pages)
         self.stats["migrations_in"] += len(recvs)
         self.stats["migrated_bytes"] += nbytes
+        self.stats["launches"] += len(sends) + len(recvs)
         for rid, r, L in ev.admitted:
             if r == me:
-                self.pages[rid] = self.ops.alloc(self.pool, -(-L // PAGE))   # prefill not emulated
+                self._add(rid, self.ops.alloc(self.pool, -(-L // PAGE)))   # prefill not emulated
 
 
 class DeviceOps:
@@ -331,6 +381,16 @@ class DeviceOps:
 
     def free(self, pool, pages):
         pool["alloc"].free(pages)
+
+    def make_table(self, slots, max_pages):
+        return self.torch.zeros(slots * max_pages, dtype=self.torch.int32, device=self.device)
+
+    def table_update(self, table, pos, val):
+        """Scatter this step's page-id deltas into the device block table (pinned H2D, async)."""
+        torch = self.torch
+        p = torch.from_numpy(pos).pin_memory().to(self.device, non_blocking=True)
+        v = torch.from_numpy(val).pin_memory().to(self.device, non_blocking=True)
+        table.index_copy_(0, p, v)
 
     def transfer(self, pool, sends, recvs, comm, page_map):
         """Pack outgoing pages, exchange with batched NCCL P2P, unpack into newly allocated

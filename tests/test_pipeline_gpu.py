@@ -71,10 +71,14 @@ def _attention_check(rt, shape, q):
 
 def test_two_instances_loopback_migration():
     shape = synth.AttnShape("t", 8, 2)
-    stages = [(0, 1200, 1), (1200, 1 << 20, 1)]
-    sim = pipeline.ClusterSim(stages, concurrency=40, seed=2, token_budget=300_000, batch_cap=128)
+    # put the stage boundary just above the median resident length so handovers happen soon
+    probe = pipeline.ClusterSim([(0, 1 << 21, 2)], concurrency=40, seed=2, token_budget=10 ** 9, batch_cap=128)
+    Ls = sorted(q.L for q in probe.reqs.values())
+    cut = Ls[len(Ls) // 2] + 8
+    stages = [(0, cut, 1), (cut, 1 << 21, 1)]
+    sim = pipeline.ClusterSim(stages, concurrency=40, seed=2, token_budget=10 ** 9, batch_cap=128)
     ops = pipeline.DeviceOps(shape, "cuda", seed=1)
-    rts = [pipeline.RankRuntime(sim, r, 300_000 // 16 * 2, shape, ops) for r in range(2)]
+    rts = [pipeline.RankRuntime(sim, r, 60000, shape, ops) for r in range(2)]
     hub = _Hub()
     q = torch.randn(128, shape.num_q_heads, 128, device="cuda").to(torch.bfloat16)
     n_mig = 0
