@@ -54,6 +54,18 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def measured_traffic(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one decode_kernel launch from the
+    committed ncu --set full capture (profiles/*_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        d = json.load(open(f))
+        if workload in d:
+            return int(d[workload]["traffic"]), os.path.relpath(f, ROOT)
+    return None, None
+
+
 def kv_bytes(lens, shape) -> int:
     return int(4 * shape.num_kv_heads * shape.head_dim * int(np.sum(lens)))
 
@@ -317,6 +329,62 @@ def mixed_vs_binned(steps: int, warmup: int):
     return res
 
 
+def heterogeneity_slowdown(steps: int, warmup: int):
+    """Fig. 2 (`fig:interference`) analogue on our kernel: batch 512,
+    k long requests among short ones (1000 vs 50000 and 200 vs 10000) against a homogeneous
+    batch with the same batch size and the same total tokens.  The paper measured 1.1-2.1x
+    slowdowns on H100 with FlashAttention / FlashInfer / Triton."""
+    import torch
+    out = []
+    for short, long in ((1000, 50000), (200, 10000)):
+        for k in (1, 8, 32):
+            mixed = synth.lengths_fig2(512, k, short, long)
+            homo = np.full(512, int(round(mixed.sum() / 512)), dtype=np.int64)
+            row = dict(short=short, long=long, n_long=k, sum_len=int(mixed.sum()))
+            for name, lens in (("mixed", mixed), ("homogeneous", homo)):
+                w = Workload(name, lens, synth.SHAPE_LLAMA3_8B)
+                t, _, _ = time_steps(w, steps, warmup)
+                row[name + "_us"] = round(t / steps * 1e3, 2)
+                row[name + "_gbs"] = round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1)
+                del w
+                torch.cuda.empty_cache()
+            row["slowdown"] = round(row["mixed_us"] / row["homogeneous_us"], 3)
+            out.append(row)
+    return out
+
+
+def migration_bandwidth(reps: int = 5):
+    """l4_migrate of one request at the Llama-3-8B shape with all 32 layers:
+    a 2048-token request = 128 pages x 32 layers x (K, V) = 256 MiB.  Loopback on one GPU
+    (HBM -> HBM: every byte read and written once); over NVLink the same kernel writes to
+    IPC-mapped peer pools."""
+    import torch
+    from paper_2512_19179_b200 import l4
+    layers, pages, n = 32, 2048, 128
+    k = torch.empty(layers, pages, 8, 16, 128, dtype=torch.bfloat16, device="cuda")
+    v = torch.empty_like(k)
+    k2, v2 = torch.empty_like(k), torch.empty_like(v)
+    src, dst = l4.kv_view(k, v, num_layers=layers), l4.kv_view(k2, v2, num_layers=layers)
+    sp = np.random.default_rng(0).permutation(pages)[:n]
+    nbytes = n * layers * 2 * src.page_bytes
+    times = []
+    for i in range(reps + 2):
+        pool = l4.PagePool(pages)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        l4.migrate(src, sp, dst, pool)
+        e1.record()
+        e1.synchronize()
+        if i >= 2:
+            times.append(e0.elapsed_time(e1))
+    t = float(np.median(times))
+    del k, v, k2, v2
+    torch.cuda.empty_cache()
+    return dict(request_tokens=n * 16, layers=layers, bytes=int(nbytes), ms=round(t, 4),
+                gbs_moved=round(nbytes / (t / 1e3) / 1e9, 1), gbs_hbm_traffic=round(2 * nbytes / (t / 1e3) / 1e9, 1),
+                note="loopback src->dst on one GPU; HBM traffic = read + write")
+
+
 # ----------------------------------------------------------------------------- pipeline (N > 1)
 def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, seed=0, shape=None):
     """C5: the length-aware pipeline on `world` GPUs.  Every step each rank runs the hot path
@@ -555,11 +623,14 @@ def main():
     extra = {}
     if rank == 0 and ws == 1 and not args.no_extra:
         extra = mixed_vs_binned(max(5, args.steps // 2), 3)
+        extra["fig2_heterogeneity"] = heterogeneity_slowdown(max(5, args.steps // 2), 3)
+        extra["migration"] = migration_bandwidth()
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(args.workload, budget_s=15.0)
     if rank != 0:
         return 0
+    traffic, traffic_src = measured_traffic(args.workload)
     line = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -583,7 +654,8 @@ def main():
         "tokens_per_s": round(ws * len(wl.lens) / (ms_step / 1e3), 1),
         "pct_hbm_peak": round(100.0 * value / (ws * peak), 2),
         "roofline": {"bound": "hbm", "kernel": "decode_kernel (l4_decode_run)", "achieved": round(achieved, 1),
-                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": peak_src, "launch_ms": round(run_avg, 5),
                      "bytes_per_launch": wl.bytes_algo},
         "e2e": {"value": round(ws * wl.bytes_kv / (e2e_step / 1e3) / 1e9, 1), "unit": "GB/s",
