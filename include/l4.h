@@ -60,7 +60,10 @@ const char* l4_version(void);
  * Layout (Z19): K and V pools are separate bf16 arrays [num_pages, Hkv, 16, 128]
  * ("HND": each (page, kv head) slice is 16 x 128 bf16 = 4 KB contiguous).
  * q is bf16 [B, Hq, 128]; out is [B, Hq, 128] f32 or bf16; lse f32 [B, Hq].
- * Page table: CSR, int32 indptr [B+1] and indices [indptr[B]]; kv_len int32 [B].
+ * Page table: int32 indptr [B+1], indices, kv_len [B].  Request b's page ids are
+ * indices[indptr[b] .. indptr[b] + ceil(L_b/16)); only those entries are read, so a
+ * compact CSR (indptr non-decreasing) and a fixed-stride block table
+ * (indptr[b] = slot_b * max_pages) are both valid.
  *
  * Method (the paper's problem, B200 design in DESIGN.md §Kernels): a device
  * planner builds LENGTH-BINNED work lists (each request's pages are split
@@ -82,8 +85,9 @@ typedef struct {
   int32_t page_size;      /* must be 16  (else L4_ERR_UNSUPPORTED) */
   float   sm_scale;       /* <= 0 -> 1/sqrt(head_dim) (Z17) */
   int32_t out_dtype;      /* L4_DT_F32 (parity) or L4_DT_BF16 */
-  int32_t chunk_pages;    /* 0 = automatic length-binned split; > 0 forces the
-                             split chunk (pages per work item); < 0 = never split */
+  int32_t chunk_pages;    /* 0 = automatic length-binned split; > 0 forces the split
+                             chunk C (pages per work item); < 0 = never split.  Requests
+                             of <= 2C pages are never split (no combine needed). */
 } l4_decode_params;
 
 /* Bytes of device workspace needed for any batch whose page table has at most
@@ -138,7 +142,7 @@ l4_status l4_decode_plan_items(const void* workspace, int32_t* items_out, int32_
  * Eq. (1) and cut cost c_{l'} = straddling tokens * bytes / bandwidth
  * (P:341).  Requests are members of the range of their final length I+O (Z4),
  * sorted by (I+O, I, index) (Z6).  Ties: smaller e', then smaller l' (Z11),
- * then fewer stages (Z12).  Bit-exact with oracle/partition.py (Z14).
+ * then fewer stages (Z12).  Bit-exact with oracle/partition.py (Z14) for every algorithm.
  * ======================================================================== */
 
 typedef struct {
@@ -156,7 +160,9 @@ typedef struct {
   int64_t kv_bytes_per_token;   /* >= 0, e.g. 2*Hkv*D*2*layers */
   double  qoe_d[5];             /* D_0..D_4 of Eq. (1) */
   int32_t stage_cost_mode;      /* 0 = paper-literal footnote (Z5/Z7); 1 = exact strided split */
-  int32_t chain;                /* 1 = one instance per stage (simplified DP) */
+  int32_t algorithm;            /* 0 = exact DP (default); 1 = chain DP, one instance per stage;
+                                   2 = two-phase heuristic: chain DP + greedy adjacent merges with the
+                                   largest positive gain, max-heap (readings Z31-Z33) */
 } l4_partition_params;
 
 /* input_len/output_len: host int64 [n], each >= 1.  stages_out: capacity >= E.

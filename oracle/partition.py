@@ -281,3 +281,51 @@ def plan_bruteforce(I, O, E, D, bandwidth, kv_bytes_per_token, edges=None, mode:
                 elif acc == best:
                     n_best += 1
     return best_plan, best, n_best
+
+
+# ---------------------------------------------------------------- two-phase heuristic
+
+def plan_two_phase(I, O, E, D, bandwidth, kv_bytes_per_token, edges=None, mode: int = 0):
+    """"We first run a simplified DP that assigns exactly one instance per stage,
+    yielding an initial E-stage pipeline ... We then iteratively merge adjacent stages to
+    reduce total latency. For each pair, we define a merge gain — the reduction in latency
+    from unifying their instance and sequence range — and greedily merge the pair with the
+    highest positive gain ... until no further improvement is possible."
+
+    Readings (Z31-Z33):
+      Z31 phase 1 is the chain DP with E1 = min(E, J) single-instance stages (J = number of
+          buckets); if E > J, each remaining instance goes to the stage whose cost drops most
+          when it gains one instance (ties: leftmost stage).
+      Z32 merge gain of adjacent stages A, B = ((cost(A) + cost(B)) + c(B.lo)) - cost(A u B),
+          A u B covering [A.lo, B.hi) with m_A + m_B instances; the pair with the largest
+          strictly positive gain is merged first (ties: leftmost pair).
+      Z33 the reported objective is recomputed from the final plan in the DP's summation order.
+    This is the obviously-correct naive O(E^2) scan; the library uses a max-heap.
+    """
+    p = _Problem(I, O, E, D, bandwidth, kv_bytes_per_token, edges, mode)
+    J = len(p.edges) - 1
+    E1 = min(p.E, J)
+    stages, _ = plan_dp(I, O, E1, D, bandwidth, kv_bytes_per_token, edges=p.edges, mode=mode, chain=True)
+    pos = {e: k for k, e in enumerate(p.edges)}
+    st = [[pos[lo], pos[hi], m] for lo, hi, m in stages]
+    for _ in range(p.E - E1):                       # Z31: place the remaining instances
+        best, best_k = None, None
+        for k, (a, b, m) in enumerate(st):
+            g = p.stage(a, b, m) - p.stage(a, b, m + 1)
+            if best is None or g > best:
+                best, best_k = g, k
+        st[best_k][2] += 1
+    while len(st) > 1:                              # Z32: greedy adjacent merges
+        best, best_k = 0.0, None
+        for k in range(len(st) - 1):
+            (a, b, m1), (b2, c, m2) = st[k], st[k + 1]
+            before = (p.stage(a, b, m1) + p.stage(b2, c, m2)) + p.cut(b2)
+            gain = before - p.stage(a, c, m1 + m2)
+            if gain > best:
+                best, best_k = gain, k
+        if best_k is None:
+            break
+        (a, _, m1), (_, c, m2) = st[best_k], st[best_k + 1]
+        st[best_k:best_k + 2] = [[a, c, m1 + m2]]
+    plan = [(p.edges[a], p.edges[b], m) for a, b, m in st]
+    return plan, plan_objective(plan, I, O, D, bandwidth, kv_bytes_per_token, edges=p.edges, mode=mode)

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <limits>
 #include <numeric>
+#include <queue>
 #include <vector>
 
 #include "l4_internal.h"
@@ -39,7 +40,7 @@ struct Stats {  // exact integer features of a request subset
 class Partitioner {
  public:
   Partitioner(const l4_partition_params& p, std::vector<Req> reqs, std::vector<int64_t> edges)
-      : E_(p.num_instances), mode_(p.stage_cost_mode), chain_(p.chain != 0), kvb_(p.kv_bytes_per_token),
+      : E_(p.num_instances), mode_(p.stage_cost_mode), kvb_(p.kv_bytes_per_token),
         bw_(p.migrate_bandwidth_Bps), reqs_(std::move(reqs)), edges_(std::move(edges)) {
     for (int k = 0; k < 5; ++k) D_[k] = p.qoe_d[k];
     // Step 4 (Z6): sort by (Lf, I, input index).
@@ -117,33 +118,27 @@ class Partitioner {
     return acc;
   }
 
-  l4_status run(l4_stage* stages_out, int32_t* num_stages_out, double* objective_out) {
-    const int E = E_, J = J_;
+  // Exact DP (or chain DP) over E instances: stages and objective (min over s of f_{s,E,J}).
+  bool dp(int E, bool chain, std::vector<l4_stage>* out, double* obj) const {
+    const int J = J_;
     const size_t SE = (size_t)(E + 1), SJ = (size_t)(J + 1);
     auto at = [&](int s, int e, int j) { return ((size_t)s * SE + (size_t)e) * SJ + (size_t)j; };
     std::vector<double> f(SE * SE * SJ, kInf);
     std::vector<int32_t> arg_e(SE * SE * SJ, -1), arg_j(SE * SE * SJ, -1);
-    // stage cost table [jp][j][m]
-    std::vector<double> st((size_t)SJ * SJ * SE, 0.0);
-    auto sti = [&](int jp, int j, int m) { return ((size_t)jp * SJ + (size_t)j) * SE + (size_t)m; };
-    for (int jp = 0; jp < J; ++jp)
-      for (int j = jp + 1; j <= J; ++j)
-        for (int m = 1; m <= E; ++m) st[sti(jp, j, m)] = stage(jp, j, m);
-
     f[at(0, 0, 0)] = 0.0;
     for (int s = 1; s <= E; ++s) {
       for (int e = s; e <= E; ++e) {
         for (int j = 1; j <= J; ++j) {
           double best = kInf;
           int be = -1, bj = -1;
-          const int ep_lo = chain_ ? e - 1 : s - 1;
+          const int ep_lo = chain ? e - 1 : s - 1;
           for (int ep = ep_lo; ep <= e - 1; ++ep) {  // Z1: e' <= e-1
             if (ep < s - 1) continue;
             const int m = e - ep;
             for (int jp = 0; jp < j; ++jp) {
               const double prev = f[at(s - 1, ep, jp)];
               if (prev == kInf) continue;
-              const double v = (prev + st[sti(jp, j, m)]) + cut_[jp];
+              const double v = (prev + st_[sti(jp, j, m)]) + cut_[jp];
               if (v < best) {  // Z11: first strict minimum
                 best = v;
                 be = ep;
@@ -165,26 +160,122 @@ class Partitioner {
         best_s = s;
       }
     }
-    if (best_s < 0) return l4::fail(L4_ERR_INFEASIBLE, "l4_partition: no feasible plan");
-    std::vector<l4_stage> out;
+    if (best_s < 0) return false;
+    out->clear();
     int s = best_s, e = E, j = J;
     while (s > 0) {
       const int ep = arg_e[at(s, e, j)], jp = arg_j[at(s, e, j)];
-      out.push_back(l4_stage{edges_[jp], edges_[j], (int32_t)(e - ep)});
+      out->push_back(l4_stage{jp, j, (int32_t)(e - ep)});  // edge indices for now
       s -= 1;
       e = ep;
       j = jp;
     }
-    std::reverse(out.begin(), out.end());
-    for (size_t k = 0; k < out.size(); ++k) stages_out[k] = out[k];
-    *num_stages_out = (int32_t)out.size();
-    *objective_out = best;
+    std::reverse(out->begin(), out->end());
+    *obj = best;
+    return true;
+  }
+
+  // Objective of a plan given as edge-index stages, in the DP's summation order.
+  double objective(const std::vector<l4_stage>& plan) const {
+    double acc = 0.0;
+    for (const l4_stage& x : plan) acc = (acc + stage_cost((int)x.lo, (int)x.hi, x.instances)) + cut_[x.lo];
+    return acc;
+  }
+
+  double stage_cost(int jp, int j, int m) const { return m <= E_ ? st_[sti(jp, j, m)] : stage(jp, j, m); }
+
+  // P:360-362 two-phase heuristic (readings Z31-Z33): chain DP over min(E, J) single-instance
+  // stages, top-up of the remaining instances, then greedy merging of the adjacent pair with the
+  // largest positive gain, tracked in a max-heap with lazy invalidation.
+  bool two_phase(std::vector<l4_stage>* out, double* obj) const {
+    const int E1 = std::min(E_, J_);
+    std::vector<l4_stage> plan;
+    double unused;
+    if (!dp(E1, true, &plan, &unused)) return false;
+    for (int extra = E1; extra < E_; ++extra) {  // Z31
+      int best_k = -1;
+      double best = 0.0;
+      for (size_t k = 0; k < plan.size(); ++k) {
+        const double g = stage_cost((int)plan[k].lo, (int)plan[k].hi, plan[k].instances) -
+                         stage_cost((int)plan[k].lo, (int)plan[k].hi, plan[k].instances + 1);
+        if (best_k < 0 || g > best) {
+          best = g;
+          best_k = (int)k;
+        }
+      }
+      plan[(size_t)best_k].instances += 1;
+    }
+    // doubly linked list of stages with versions; heap of (gain, -lo) with lazy invalidation (Z32)
+    const int n = (int)plan.size();
+    std::vector<int> prev(n), next(n), ver(n, 0);
+    std::vector<char> alive(n, 1);
+    for (int k = 0; k < n; ++k) {
+      prev[k] = k - 1;
+      next[k] = k + 1 < n ? k + 1 : -1;
+    }
+    struct Entry {
+      double gain;
+      int64_t lo;
+      int left, right, vl, vr;
+      bool operator<(const Entry& o) const {  // max gain first, then leftmost
+        if (gain != o.gain) return gain < o.gain;
+        return lo > o.lo;
+      }
+    };
+    std::priority_queue<Entry> heap;
+    auto gain_of = [&](int a, int b) {
+      const l4_stage& A = plan[(size_t)a];
+      const l4_stage& B = plan[(size_t)b];
+      const double before = (stage_cost((int)A.lo, (int)A.hi, A.instances) +
+                             stage_cost((int)B.lo, (int)B.hi, B.instances)) + cut_[B.lo];
+      return before - stage_cost((int)A.lo, (int)B.hi, A.instances + B.instances);
+    };
+    auto push = [&](int a) {
+      const int b = next[a];
+      if (a < 0 || b < 0) return;
+      const double g = gain_of(a, b);
+      if (g > 0.0) heap.push(Entry{g, plan[(size_t)a].lo, a, b, ver[a], ver[b]});
+    };
+    for (int k = 0; k + 1 < n; ++k) push(k);
+    while (!heap.empty()) {
+      const Entry t = heap.top();
+      heap.pop();
+      if (!alive[t.left] || !alive[t.right] || next[t.left] != t.right || ver[t.left] != t.vl || ver[t.right] != t.vr)
+        continue;  // stale
+      plan[(size_t)t.left].hi = plan[(size_t)t.right].hi;
+      plan[(size_t)t.left].instances += plan[(size_t)t.right].instances;
+      ver[t.left] += 1;
+      alive[t.right] = 0;
+      next[t.left] = next[t.right];
+      if (next[t.right] >= 0) prev[next[t.right]] = t.left;
+      if (prev[t.left] >= 0) push(prev[t.left]);
+      push(t.left);
+    }
+    out->clear();
+    for (int k = 0; k >= 0 && k < n; k = next[k]) out->push_back(plan[(size_t)k]);
+    *obj = objective(*out);  // Z33
+    return true;
+  }
+
+  l4_status run(int algorithm, l4_stage* stages_out, int32_t* num_stages_out, double* objective_out) {
+    // stage cost table [jp][j][m] for m = 1..E
+    st_.assign((size_t)(J_ + 1) * (J_ + 1) * (E_ + 1), 0.0);
+    for (int jp = 0; jp < J_; ++jp)
+      for (int j = jp + 1; j <= J_; ++j)
+        for (int m = 1; m <= E_; ++m) st_[sti(jp, j, m)] = stage(jp, j, m);
+    std::vector<l4_stage> plan;
+    double obj = 0.0;
+    bool ok = algorithm == 2 ? two_phase(&plan, &obj) : dp(E_, algorithm == 1, &plan, &obj);
+    if (!ok) return l4::fail(L4_ERR_INFEASIBLE, "l4_partition: no feasible plan");
+    for (size_t k = 0; k < plan.size(); ++k)
+      stages_out[k] = l4_stage{edges_[(size_t)plan[k].lo], edges_[(size_t)plan[k].hi], plan[k].instances};
+    *num_stages_out = (int32_t)plan.size();
+    *objective_out = obj;
     return L4_OK;
   }
 
  private:
   int E_, mode_;
-  bool chain_;
   int64_t kvb_;
   double bw_;
   double D_[5];
@@ -193,8 +284,12 @@ class Partitioner {
   std::vector<int64_t> pos_;
   std::vector<std::vector<Stats>> pref_;
   std::vector<double> cut_;
+  std::vector<double> st_;
   int64_t n_ = 0;
   int J_ = 0;
+  size_t sti(int jp, int j, int m) const {
+    return ((size_t)jp * (size_t)(J_ + 1) + (size_t)j) * (size_t)(E_ + 1) + (size_t)m;
+  }
 };
 
 }  // namespace
@@ -236,6 +331,7 @@ extern "C" l4_status l4_partition(const l4_partition_params* p, const int64_t* i
     if (edges.back() <= max_lf) return l4::fail(L4_ERR_INFEASIBLE, "l4_partition: top edge must exceed max(I+O)");
   }
   if (edges.size() > 4096) return l4::fail(L4_ERR_UNSUPPORTED, "l4_partition: too many edges");
+  L4_CHECK_ARG(p->algorithm >= 0 && p->algorithm <= 2, "l4_partition: algorithm must be 0, 1 or 2");
   Partitioner part(*p, std::move(reqs), std::move(edges));
-  return part.run(stages_out, num_stages_out, objective_out);
+  return part.run(p->algorithm, stages_out, num_stages_out, objective_out);
 }

@@ -59,7 +59,7 @@ class PartitionParams(ctypes.Structure):
     _fields_ = [("num_instances", ctypes.c_int32), ("edges", ctypes.POINTER(ctypes.c_int64)),
                 ("num_edges", ctypes.c_int32), ("migrate_bandwidth_Bps", ctypes.c_double),
                 ("kv_bytes_per_token", ctypes.c_int64), ("qoe_d", ctypes.c_double * 5),
-                ("stage_cost_mode", ctypes.c_int32), ("chain", ctypes.c_int32)]
+                ("stage_cost_mode", ctypes.c_int32), ("algorithm", ctypes.c_int32)]
 
 
 class KVView(ctypes.Structure):
@@ -244,9 +244,14 @@ def plan_items(workspace, stream=None) -> np.ndarray:
 
 # --------------------------------------------------------------------------- partition (host)
 
+PART_EXACT, PART_CHAIN, PART_TWO_PHASE = 0, 1, 2
+
+
 def partition(input_len: Sequence[int], output_len: Sequence[int], num_instances: int, qoe_d,
-              bandwidth_Bps: float, kv_bytes_per_token: int, edges=None, mode: int = 0, chain: bool = False):
-    """l4_partition: returns ([(lo, hi, instances)], objective)."""
+              bandwidth_Bps: float, kv_bytes_per_token: int, edges=None, mode: int = 0, chain: bool = False,
+              algorithm: int = PART_EXACT):
+    """l4_partition: returns ([(lo, hi, instances)], objective).  algorithm: 0 exact DP,
+    1 chain DP (also selected by chain=True), 2 two-phase heuristic."""
     I = np.ascontiguousarray(np.asarray(input_len, dtype=np.int64))
     O = np.ascontiguousarray(np.asarray(output_len, dtype=np.int64))
     if I.shape != O.shape:
@@ -263,7 +268,7 @@ def partition(input_len: Sequence[int], output_len: Sequence[int], num_instances
     for k in range(5):
         p.qoe_d[k] = float(qoe_d[k])
     p.stage_cost_mode = int(mode)
-    p.chain = 1 if chain else 0
+    p.algorithm = PART_CHAIN if chain else int(algorithm)
     cap = max(int(num_instances), 1)
     stages = (Stage * cap)()
     ns = ctypes.c_int32(0)

@@ -176,3 +176,36 @@ def test_decode_param_validation():
         p = l4.make_params(**args)
         st = L.l4_decode_plan(p, None, None, 0, None, 0, None)
         assert st == status, (kw, st, L.l4_last_error())
+
+
+def test_two_phase_bit_exact_with_oracle():
+    rng = np.random.default_rng(77)
+    n_merged = 0
+    for case in range(80):
+        n = int(rng.integers(0, 60))
+        I = rng.integers(1, int(rng.choice([30, 600, 5000])), size=n).tolist()
+        O = rng.integers(1, int(rng.choice([30, 600, 5000])), size=n).tolist()
+        D = tuple(float(x) for x in rng.random(5) * np.array([1e-2, 1e-4, 1e-6, 1e-9, 1e-5]))
+        E = int(rng.integers(1, 24))                  # also E > number of buckets (Z31 top-up)
+        bw = float(rng.uniform(1e2, 1e9))
+        kvb = int(rng.integers(0, 200000))
+        for mode in (0, 1):
+            ref = op.plan_two_phase(I, O, E, D, bw, kvb, mode=mode)
+            got = l4.partition(I, O, E, D, bw, kvb, mode=mode, algorithm=l4.PART_TWO_PHASE)
+            assert got[0] == ref[0], (case, mode)
+            assert got[1] == ref[1]
+            n_merged += len(ref[0]) < min(E, 99)
+    assert n_merged > 10
+
+
+def test_two_phase_scale_and_quality():
+    """At the paper's planner setting (E = 16, 128K contexts) the heuristic is fast and
+    never better than the exact DP."""
+    I, O = synth.requests_sharegpt_like(seed=2, n=10000)
+    D = synth.roofline_qoe_d()
+    t = time.perf_counter()
+    plan, obj = l4.partition(I, O, 16, D, 7e11, 131072, algorithm=l4.PART_TWO_PHASE)
+    dt = time.perf_counter() - t
+    _, exact = l4.partition(I, O, 16, D, 7e11, 131072)
+    assert obj >= exact and dt < 1.0
+    assert sum(m for _, _, m in plan) == 16

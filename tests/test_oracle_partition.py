@@ -236,3 +236,37 @@ def test_modes_agree_at_scale():
     s1, _ = op.plan_dp(I, O, 4, D, 7e11, 131072, mode=1)
     assert s0 == s1
     assert 2 <= len(s0) <= 4
+
+
+def test_two_phase_never_beats_exact_and_merges_help():
+    """Heuristic objective >= exact optimum; merging never increases the chain objective."""
+    rng = np.random.default_rng(21)
+    for _ in range(25):
+        I, O, D, bw, kvb = _random_workload(rng, small_edges=False)
+        E = int(rng.integers(1, 9))
+        for mode in (0, 1):
+            plan, obj = op.plan_two_phase(I, O, E, D, bw, kvb, mode=mode)
+            _, exact = op.plan_dp(I, O, E, D, bw, kvb, mode=mode)
+            assert obj >= exact
+            assert sum(m for _, _, m in plan) == E
+            edges = op.default_edges(max([i + o for i, o in zip(I, O)], default=0))
+            J = len(edges) - 1
+            if E <= J:
+                _, chain = op.plan_dp(I, O, E, D, bw, kvb, mode=mode, chain=True)
+                assert obj <= chain
+            assert obj == op.plan_objective(plan, I, O, D, bw, kvb, mode=mode)
+
+
+def test_two_phase_merges_when_cut_cost_dominates():
+    """S:258 example: two stages whose migration cost at the cut dominates are merged into one."""
+    I = [1, 2, 3, 40, 41, 42]
+    O = [60, 60, 60, 2, 2, 2]                       # the short-input requests straddle every cut
+    D = (0.0, 0.0, 0.0, 0.0, 1e-3)
+    plan, obj = op.plan_two_phase(I, O, 2, D, 1.0, 10 ** 6)
+    assert plan == [(0, 64, 2)]                     # one stage, no cut to pay
+    # and with free migration the chain's two stages are kept
+    # two well-separated groups and no straddlers: the chain's two stages are kept
+    # (chain: 3*30 + 3*300 = 990 < merged 2 * 3 * (10 + 100 + 100) = 1260, D4 = 1)
+    I2, O2 = [5, 5, 5, 50, 50, 50], [5, 5, 5, 50, 50, 50]
+    plan2, obj2 = op.plan_two_phase(I2, O2, 2, (0, 0, 0, 0, 1.0), 1.0, 1)
+    assert plan2 == [(0, 16, 1), (16, 128, 1)] and obj2 == 990.0
