@@ -172,6 +172,25 @@ typedef struct {
 l4_status l4_partition(const l4_partition_params* p, const int64_t* input_len, const int64_t* output_len,
                        int64_t n, l4_stage* stages_out, int32_t* num_stages_out, double* objective_out);
 
+/* §4.3 adaptive range refinement (readings Z34-Z37): refine the boundary
+ * between a stage [lo, boundary) and its successor [boundary, hi).  The successors'
+ * (I, L) sets (CSR: succ_indptr [n_succ+1], succ_I / succ_L) are averaged with the
+ * §4.2 set division, merged with the local (I, L) list and sorted by (L, I) into R;
+ * b = argmin_{0<=i<N} Q^{R[:i]} + Q^{R[i:]} (Eq. (1), smallest i on ties); the boundary
+ * moves by an exponential moving average towards R[b].L and is clamped to
+ * [lo+1, hi-1].  With fewer than min_traffic merged requests it is left unchanged
+ * (raw_out = split_out = -1).  Bit-exact with oracle/refine.py. */
+typedef struct {
+  double  qoe_d[5];       /* D_0..D_4 of Eq. (1) */
+  double  ema_alpha;      /* in [0, 1] */
+  int32_t min_traffic;    /* freeze below this many requests (paper: five) */
+  int64_t lo, hi;         /* outer bounds: the stage's lo and the successor stage's hi */
+} l4_refine_params;
+l4_status l4_refine_boundary(const l4_refine_params* p, const int64_t* local_I, const int64_t* local_L,
+                             int64_t n_local, int32_t n_succ, const int64_t* succ_indptr, const int64_t* succ_I,
+                             const int64_t* succ_L, double boundary_in, double* boundary_out, int64_t* raw_out,
+                             int64_t* split_out);
+
 /* ========================================================================
  * 3. KV page pool and migration
  * ======================================================================== */

@@ -335,3 +335,87 @@ extern "C" l4_status l4_partition(const l4_partition_params* p, const int64_t* i
   Partitioner part(*p, std::move(reqs), std::move(edges));
   return part.run(p->algorithm, stages_out, num_stages_out, objective_out);
 }
+
+// ===================================================================== §4.3 refinement
+// l4_refine_boundary (include/l4.h): P:369-379, readings Z34-Z37.  The argmin over all
+// split points of the merged sorted list uses int64 prefix sums, so each candidate's
+// Q^{R[:i]} + Q^{R[i:]} is computed from exact integer features in the oracle's order.
+namespace {
+
+struct Seq {
+  int64_t I, L;
+};
+
+double qoe_of(const double* D, int64_t n, int64_t sI, int64_t sI2, int64_t sL) {
+  if (n == 0) return 0.0;
+  double q = D[0] * 1.0;
+  q = q + D[1] * (double)n;
+  q = q + D[2] * (double)sI;
+  q = q + D[3] * (double)sI2;
+  q = q + D[4] * (double)sL;
+  return (double)n * q;
+}
+
+bool seq_less(const Seq& a, const Seq& b) { return a.L != b.L ? a.L < b.L : a.I < b.I; }
+
+}  // namespace
+
+extern "C" l4_status l4_refine_boundary(const l4_refine_params* p, const int64_t* local_I, const int64_t* local_L,
+                                        int64_t n_local, int32_t n_succ, const int64_t* succ_indptr,
+                                        const int64_t* succ_I, const int64_t* succ_L, double boundary_in,
+                                        double* boundary_out, int64_t* raw_out, int64_t* split_out) {
+  L4_CHECK_ARG(p && boundary_out && raw_out && split_out, "l4_refine_boundary: NULL argument");
+  L4_CHECK_ARG(n_local >= 0 && n_succ >= 0, "l4_refine_boundary: negative count");
+  L4_CHECK_ARG(n_local == 0 || (local_I && local_L), "l4_refine_boundary: local arrays NULL");
+  L4_CHECK_ARG(n_succ == 0 || succ_indptr, "l4_refine_boundary: succ_indptr NULL");
+  L4_CHECK_ARG(p->ema_alpha >= 0.0 && p->ema_alpha <= 1.0, "l4_refine_boundary: ema_alpha must be in [0, 1]");
+  L4_CHECK_ARG(p->hi - p->lo >= 2, "l4_refine_boundary: need hi - lo >= 2");
+  L4_CHECK_ARG(std::isfinite(boundary_in), "l4_refine_boundary: boundary must be finite");
+  // successor average: canonical subset of the sorted union (Z35)
+  std::vector<Seq> uni;
+  if (n_succ > 0) {
+    L4_CHECK_ARG(succ_indptr[0] == 0, "l4_refine_boundary: succ_indptr[0] must be 0");
+    for (int32_t k = 0; k < n_succ; ++k)
+      L4_CHECK_ARG(succ_indptr[k + 1] >= succ_indptr[k], "l4_refine_boundary: succ_indptr not monotone");
+    const int64_t tot = succ_indptr[n_succ];
+    L4_CHECK_ARG(tot == 0 || (succ_I && succ_L), "l4_refine_boundary: successor arrays NULL");
+    uni.reserve((size_t)tot);
+    for (int64_t i = 0; i < tot; ++i) uni.push_back(Seq{succ_I[i], succ_L[i]});
+    std::sort(uni.begin(), uni.end(), seq_less);
+  }
+  std::vector<Seq> R;
+  R.reserve((size_t)n_local + uni.size());
+  for (int64_t i = 0; i < n_local; ++i) R.push_back(Seq{local_I[i], local_L[i]});
+  for (size_t i = (size_t)(n_succ / 2); n_succ > 0 && i < uni.size(); i += (size_t)n_succ) R.push_back(uni[i]);
+  std::sort(R.begin(), R.end(), seq_less);
+  const int64_t N = (int64_t)R.size();
+  if (N < p->min_traffic || N == 0) {  // P:379 freeze (Z37)
+    *boundary_out = boundary_in;
+    *raw_out = -1;
+    *split_out = -1;
+    return L4_OK;
+  }
+  std::vector<int64_t> cI(N + 1, 0), cI2(N + 1, 0), cL(N + 1, 0);
+  for (int64_t i = 0; i < N; ++i) {
+    cI[i + 1] = cI[i] + R[i].I;
+    cI2[i + 1] = cI2[i] + R[i].I * R[i].I;
+    cL[i + 1] = cL[i] + R[i].L;
+  }
+  double best = std::numeric_limits<double>::infinity();
+  int64_t b = 0;
+  for (int64_t i = 0; i < N; ++i) {  // Z36: first strict minimum
+    const double v = qoe_of(p->qoe_d, i, cI[i], cI2[i], cL[i]) +
+                     qoe_of(p->qoe_d, N - i, cI[N] - cI[i], cI2[N] - cI2[i], cL[N] - cL[i]);
+    if (v < best) {
+      best = v;
+      b = i;
+    }
+  }
+  const int64_t raw = R[(size_t)b].L;
+  double nb = p->ema_alpha * (double)raw + (1.0 - p->ema_alpha) * boundary_in;
+  nb = std::min(std::max(nb, (double)(p->lo + 1)), (double)(p->hi - 1));
+  *boundary_out = nb;
+  *raw_out = raw;
+  *split_out = b;
+  return L4_OK;
+}

@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = (
     "l4_decode_attention", "l4_decode_plan_info", "l4_decode_plan_items", "l4_partition", "l4_pool_create",
     "l4_pool_alloc", "l4_pool_free", "l4_pool_num_free", "l4_pool_destroy", "l4_migrate", "l4_copy_pages",
     "l4_pack_pages", "l4_unpack_pages", "l4_ipc_get_handle", "l4_ipc_open_handle", "l4_ipc_close_handle",
-    "l4_enable_peer_access",
+    "l4_enable_peer_access", "l4_refine_boundary",
 )
 
 
@@ -60,6 +60,11 @@ class PartitionParams(ctypes.Structure):
                 ("num_edges", ctypes.c_int32), ("migrate_bandwidth_Bps", ctypes.c_double),
                 ("kv_bytes_per_token", ctypes.c_int64), ("qoe_d", ctypes.c_double * 5),
                 ("stage_cost_mode", ctypes.c_int32), ("algorithm", ctypes.c_int32)]
+
+
+class RefineParams(ctypes.Structure):
+    _fields_ = [("qoe_d", ctypes.c_double * 5), ("ema_alpha", ctypes.c_double), ("min_traffic", ctypes.c_int32),
+                ("lo", ctypes.c_int64), ("hi", ctypes.c_int64)]
 
 
 class KVView(ctypes.Structure):
@@ -122,6 +127,9 @@ def lib() -> ctypes.CDLL:
     L.l4_ipc_open_handle.argtypes = [vp, P(vp)]
     L.l4_ipc_close_handle.restype = ctypes.c_int
     L.l4_ipc_close_handle.argtypes = [vp]
+    L.l4_refine_boundary.restype = ctypes.c_int
+    L.l4_refine_boundary.argtypes = [P(RefineParams), vp, vp, i64, i32, vp, vp, vp, ctypes.c_double,
+                                     P(ctypes.c_double), P(i64), P(i64)]
     L.l4_enable_peer_access.restype = ctypes.c_int
     L.l4_enable_peer_access.argtypes = [i32]
     _lib = L
@@ -276,6 +284,30 @@ def partition(input_len: Sequence[int], output_len: Sequence[int], num_instances
     _check(lib().l4_partition(ctypes.byref(p), I.ctypes.data if I.size else None, O.ctypes.data if O.size else None,
                               int(I.size), stages, ctypes.byref(ns), ctypes.byref(obj)))
     return [(int(stages[k].lo), int(stages[k].hi), int(stages[k].instances)) for k in range(ns.value)], obj.value
+
+
+def refine_boundary(boundary: float, local, successor_sets, qoe_d, alpha: float = 0.3, min_traffic: int = 5,
+                    lo: int = 0, hi: int = 1 << 62):
+    """l4_refine_boundary: local = [(I, L)], successor_sets = [[(I, L)], ...].
+    Returns (new boundary, raw split length or None, split index or None)."""
+    loc = np.asarray(list(local), dtype=np.int64).reshape(-1, 2)
+    sets = [np.asarray(list(s), dtype=np.int64).reshape(-1, 2) for s in successor_sets]
+    indptr = np.zeros(len(sets) + 1, dtype=np.int64)
+    for k, s in enumerate(sets):
+        indptr[k + 1] = indptr[k] + len(s)
+    allsucc = np.concatenate(sets) if sets and indptr[-1] > 0 else np.zeros((0, 2), dtype=np.int64)
+    lI, lL = np.ascontiguousarray(loc[:, 0]), np.ascontiguousarray(loc[:, 1])
+    sI, sL = np.ascontiguousarray(allsucc[:, 0]), np.ascontiguousarray(allsucc[:, 1])
+    p = RefineParams()
+    for k in range(5):
+        p.qoe_d[k] = float(qoe_d[k])
+    p.ema_alpha, p.min_traffic, p.lo, p.hi = float(alpha), int(min_traffic), int(lo), int(hi)
+    out_b, raw, split = ctypes.c_double(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    ptr = lambda a: a.ctypes.data if a.size else None
+    _check(lib().l4_refine_boundary(ctypes.byref(p), ptr(lI), ptr(lL), int(lI.size), len(sets),
+                                    indptr.ctypes.data if sets else None, ptr(sI), ptr(sL), float(boundary),
+                                    ctypes.byref(out_b), ctypes.byref(raw), ctypes.byref(split)))
+    return out_b.value, (None if raw.value < 0 else int(raw.value)), (None if split.value < 0 else int(split.value))
 
 
 # --------------------------------------------------------------------------- page pool + migration

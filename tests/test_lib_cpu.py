@@ -209,3 +209,22 @@ def test_two_phase_scale_and_quality():
     _, exact = l4.partition(I, O, 16, D, 7e11, 131072)
     assert obj >= exact and dt < 1.0
     assert sum(m for _, _, m in plan) == 16
+
+
+def test_refine_boundary_bit_exact_with_oracle():
+    from oracle import refine as orf
+    rng = np.random.default_rng(31)
+    for case in range(300):
+        nl = int(rng.integers(0, 30))
+        ns = int(rng.integers(0, 4))
+        local = [(int(rng.integers(1, 400)), int(rng.integers(1, 3000))) for _ in range(nl)]
+        succ = [[(int(rng.integers(1, 400)), int(rng.integers(1000, 9000))) for _ in range(int(rng.integers(0, 20)))]
+                for _ in range(ns)]
+        D = tuple(float(x) for x in rng.random(5) * np.array([1e-2, 1e-4, 1e-6, 1e-9, 1e-5]))
+        alpha = float(rng.choice([0.0, 0.3, 1.0, rng.random()]))
+        b0 = float(rng.uniform(500, 5000))
+        mt = int(rng.integers(0, 8))
+        lo, hi = 0, int(rng.choice([2000, 10 ** 6]))
+        ref = orf.refine(b0, local, succ, D, alpha, mt, lo, hi)
+        got = l4.refine_boundary(b0, local, succ, D, alpha, mt, lo, hi)
+        assert got == ref, (case, got, ref)
