@@ -172,6 +172,15 @@ typedef struct {
 l4_status l4_partition(const l4_partition_params* p, const int64_t* input_len, const int64_t* output_len,
                        int64_t n, l4_stage* stages_out, int32_t* num_stages_out, double* objective_out);
 
+/* §4.1 QoE model fit: least-squares D_0..D_4 with Q^(j) ~ sum_k D_k F_k^(j).
+ * F: host row-major [n, 5] features (1, n, sum I, sum I^2, sum L) per sample; Q: [n] observed
+ * per-request latency.  column_mask bit k selects F_k (reading Z38: decode-only profiles use
+ * 0b10011 = {1, n, sum L}); unselected D_k = 0.  Householder QR on scaled columns.
+ * Errors: n < selected columns -> INVALID_ARG; rank deficient -> INFEASIBLE.
+ * rms_out (nullable): root-mean-square residual. */
+l4_status l4_qoe_fit(const double* F, const double* Q, int64_t n, uint32_t column_mask, double* D_out,
+                     double* rms_out);
+
 /* §4.3 adaptive range refinement (readings Z34-Z37): refine the boundary
  * between a stage [lo, boundary) and its successor [boundary, hi).  The successors'
  * (I, L) sets (CSR: succ_indptr [n_succ+1], succ_I / succ_L) are averaged with the

@@ -419,3 +419,77 @@ extern "C" l4_status l4_refine_boundary(const l4_refine_params* p, const int64_t
   *split_out = b;
   return L4_OK;
 }
+
+// ===================================================================== §4.1 QoE fit
+// l4_qoe_fit (include/l4.h): least squares Q ~ sum_k D_k F_k by Householder QR
+// on max-abs-scaled columns (features span ~12 orders of magnitude); rank < selected
+// columns -> L4_ERR_INFEASIBLE.
+extern "C" l4_status l4_qoe_fit(const double* F, const double* Q, int64_t n, uint32_t column_mask, double* D_out,
+                                double* rms_out) {
+  L4_CHECK_ARG(F && Q && D_out, "l4_qoe_fit: NULL argument");
+  int cols[5], p = 0;
+  for (int k = 0; k < 5; ++k)
+    if (column_mask & (1u << k)) cols[p++] = k;
+  L4_CHECK_ARG(p >= 1, "l4_qoe_fit: empty column mask");
+  if (n < p) return l4::fail(L4_ERR_INVALID_ARG, "l4_qoe_fit: too few samples");
+  std::vector<double> A((size_t)n * p), b(Q, Q + n), scale(p);
+  for (int c = 0; c < p; ++c) {
+    double m = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double v = F[i * 5 + cols[c]];
+      A[(size_t)c * n + i] = v;  // column-major
+      m = std::max(m, std::fabs(v));
+    }
+    if (!(m > 0.0) || !std::isfinite(m)) return l4::fail(L4_ERR_INFEASIBLE, "l4_qoe_fit: zero or non-finite column");
+    scale[c] = m;
+    for (int64_t i = 0; i < n; ++i) A[(size_t)c * n + i] /= m;
+  }
+  for (int k = 0; k < p; ++k) {  // Householder reflections
+    double* ak = &A[(size_t)k * n];
+    double norm = 0.0;
+    for (int64_t i = k; i < n; ++i) norm += ak[i] * ak[i];
+    norm = std::sqrt(norm);
+    if (norm == 0.0) return l4::fail(L4_ERR_INFEASIBLE, "l4_qoe_fit: rank deficient feature matrix");
+    const double alpha = ak[k] > 0 ? -norm : norm;
+    std::vector<double> v((size_t)(n - k));
+    for (int64_t i = k; i < n; ++i) v[(size_t)(i - k)] = ak[i];
+    v[0] -= alpha;
+    double vn = 0.0;
+    for (double x : v) vn += x * x;
+    if (vn > 0.0) {
+      for (int c = k; c < p; ++c) {
+        double* ac = &A[(size_t)c * n];
+        double dot = 0.0;
+        for (int64_t i = k; i < n; ++i) dot += v[(size_t)(i - k)] * ac[i];
+        const double f = 2.0 * dot / vn;
+        for (int64_t i = k; i < n; ++i) ac[i] -= f * v[(size_t)(i - k)];
+      }
+      double dot = 0.0;
+      for (int64_t i = k; i < n; ++i) dot += v[(size_t)(i - k)] * b[(size_t)i];
+      const double f = 2.0 * dot / vn;
+      for (int64_t i = k; i < n; ++i) b[(size_t)i] -= f * v[(size_t)(i - k)];
+    }
+  }
+  double rmax = 0.0;
+  for (int k = 0; k < p; ++k) rmax = std::max(rmax, std::fabs(A[(size_t)k * n + k]));
+  for (int k = 0; k < p; ++k)
+    if (std::fabs(A[(size_t)k * n + k]) <= 1e-10 * rmax)
+      return l4::fail(L4_ERR_INFEASIBLE, "l4_qoe_fit: rank deficient feature matrix");
+  double x[5] = {0, 0, 0, 0, 0};
+  for (int k = p - 1; k >= 0; --k) {  // back substitution R x = Q^T b
+    double s = b[(size_t)k];
+    for (int c = k + 1; c < p; ++c) s -= A[(size_t)c * n + k] * x[c];
+    x[k] = s / A[(size_t)k * n + k];
+  }
+  double D[5] = {0, 0, 0, 0, 0};
+  for (int c = 0; c < p; ++c) D[cols[c]] = x[c] / scale[c];
+  double ss = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double pred = 0.0;
+    for (int k = 0; k < 5; ++k) pred += D[k] * F[i * 5 + k];
+    ss += (Q[i] - pred) * (Q[i] - pred);
+  }
+  for (int k = 0; k < 5; ++k) D_out[k] = D[k];
+  if (rms_out) *rms_out = std::sqrt(ss / (double)n);
+  return L4_OK;
+}

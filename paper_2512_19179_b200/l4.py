@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = (
     "l4_decode_attention", "l4_decode_plan_info", "l4_decode_plan_items", "l4_partition", "l4_pool_create",
     "l4_pool_alloc", "l4_pool_free", "l4_pool_num_free", "l4_pool_destroy", "l4_migrate", "l4_copy_pages",
     "l4_pack_pages", "l4_unpack_pages", "l4_ipc_get_handle", "l4_ipc_open_handle", "l4_ipc_close_handle",
-    "l4_enable_peer_access", "l4_refine_boundary",
+    "l4_enable_peer_access", "l4_refine_boundary", "l4_qoe_fit",
 )
 
 
@@ -127,6 +127,8 @@ def lib() -> ctypes.CDLL:
     L.l4_ipc_open_handle.argtypes = [vp, P(vp)]
     L.l4_ipc_close_handle.restype = ctypes.c_int
     L.l4_ipc_close_handle.argtypes = [vp]
+    L.l4_qoe_fit.restype = ctypes.c_int
+    L.l4_qoe_fit.argtypes = [vp, vp, i64, ctypes.c_uint32, vp, P(ctypes.c_double)]
     L.l4_refine_boundary.restype = ctypes.c_int
     L.l4_refine_boundary.argtypes = [P(RefineParams), vp, vp, i64, i32, vp, vp, vp, ctypes.c_double,
                                      P(ctypes.c_double), P(i64), P(i64)]
@@ -284,6 +286,17 @@ def partition(input_len: Sequence[int], output_len: Sequence[int], num_instances
     _check(lib().l4_partition(ctypes.byref(p), I.ctypes.data if I.size else None, O.ctypes.data if O.size else None,
                               int(I.size), stages, ctypes.byref(ns), ctypes.byref(obj)))
     return [(int(stages[k].lo), int(stages[k].hi), int(stages[k].instances)) for k in range(ns.value)], obj.value
+
+
+def qoe_fit(F, Q, mask=(1, 1, 1, 1, 1)):
+    """l4_qoe_fit: returns (D[5], rms residual)."""
+    Fa = np.ascontiguousarray(np.asarray(F, dtype=np.float64).reshape(-1, 5))
+    Qa = np.ascontiguousarray(np.asarray(Q, dtype=np.float64).reshape(-1))
+    bits = sum(1 << k for k in range(5) if mask[k])
+    D = np.zeros(5)
+    rms = ctypes.c_double(0.0)
+    _check(lib().l4_qoe_fit(Fa.ctypes.data, Qa.ctypes.data, int(Qa.size), bits, D.ctypes.data, ctypes.byref(rms)))
+    return D, rms.value
 
 
 def refine_boundary(boundary: float, local, successor_sets, qoe_d, alpha: float = 0.3, min_traffic: int = 5,

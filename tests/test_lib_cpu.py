@@ -228,3 +228,37 @@ def test_refine_boundary_bit_exact_with_oracle():
         ref = orf.refine(b0, local, succ, D, alpha, mt, lo, hi)
         got = l4.refine_boundary(b0, local, succ, D, alpha, mt, lo, hi)
         assert got == ref, (case, got, ref)
+
+
+def test_qoe_fit_matches_lstsq_oracle():
+    from oracle import qoe as oq
+    rng = np.random.default_rng(12)
+    for case in range(60):
+        n = int(rng.integers(6, 80))
+        rows = []
+        for _ in range(n):
+            b = int(rng.integers(1, 300))
+            I = rng.integers(1, 8000, size=b)
+            L = I + rng.integers(1, 4000, size=b)
+            rows.append([1, b, I.sum(), (I * I).sum(), L.sum()])
+        F = np.array(rows, dtype=np.float64)
+        Dstar = np.array([2e-5, 2e-7, 1e-9, 1e-14, 6e-10]) * rng.uniform(0.5, 2, size=5)
+        Q = F @ Dstar * rng.uniform(0.97, 1.03, size=n)
+        mask = (1, 1, 1, 1, 1) if case % 2 == 0 else (1, 1, 0, 0, 1)
+        ref = oq.fit_params(F, Q, mask)
+        got, rms = l4.qoe_fit(F, Q, mask)
+        # least squares is unique but can be ill-conditioned in D: compare what is well-conditioned
+        # (fitted values and residual norm) tightly, and the coefficients loosely
+        pg, pr = F @ got, F @ ref
+        assert np.max(np.abs(pg - pr) / np.abs(Q)) < 1e-7, case    # ~ cond(F) * eps
+        rg, rr = np.linalg.norm(Q - pg), np.linalg.norm(Q - pr)
+        assert abs(rg - rr) <= 1e-7 * rr + 1e-30
+        assert abs(rms - rg / np.sqrt(n)) <= 1e-9 * rg
+        assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)) < 1e-3, (case, got, ref)
+    with pytest.raises(l4.L4Error) as e:
+        l4.qoe_fit(np.ones((3, 5)), np.ones(3))
+    assert e.value.status == l4.L4_ERR_INVALID_ARG
+    G = np.ones((10, 5))
+    with pytest.raises(l4.L4Error) as e:
+        l4.qoe_fit(G, np.ones(10))
+    assert e.value.status == l4.L4_ERR_INFEASIBLE
