@@ -124,7 +124,9 @@ typedef struct {
   int32_t num_items;      /* work items (request, kv head, page chunk) */
   int32_t chunk_pages;    /* chunk chosen by the planner */
   int32_t num_ctas;       /* persistent grid of l4_decode_run */
-  int32_t max_splits;     /* largest split count of any request */
+  int32_t max_splits;     /* largest split count of any request (before the guided tail) */
+  int32_t tail_requests;  /* requests of the guided tail (split finer, processed last) */
+  int32_t tail_chunk_pages; /* chunk of the guided tail (0 if none) */
 } l4_plan_info;
 l4_status l4_decode_plan_info(const void* workspace, l4_plan_info* info_out, void* stream);
 

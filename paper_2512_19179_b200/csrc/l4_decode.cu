@@ -61,6 +61,12 @@ constexpr int kMaxSplits = 512;                       // per (request, kv head);
 constexpr int kMinChunk = 8;                          // pages
 constexpr int kItemsPerCta = 8;                       // automatic chunk target
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
+// Guided tail (planner): split the last requests of the LPT order into chunks of ~per-CTA/16.
+// Measured r1: with the synchronous split epilogue it costs more than it saves (C2 151 -> 164 us),
+// so it is disabled (kTailChunksPerCta = 0) until the epilogue is asynchronous.
+constexpr int kTailChunksPerCta = 0;
+constexpr int kTailDiv = 16;
+constexpr int kMinTailChunk = 4;                      // pages
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
 constexpr int kNumBins = 32;
@@ -76,7 +82,7 @@ static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
 struct __align__(16) PlanHeader {
   int n_items, chunk, num_ctas, max_splits;
   int batch, num_kv_heads, items_cap, pad;
-  int pad2[8];
+  int tail_requests, tail_chunk, pad2[6];
   int sched_next, sched_done, pad3[14];  // ticket counter and finished-CTA count (self-resetting)
 };
 static_assert(sizeof(PlanHeader) == 128, "PlanHeader is 128 bytes");
@@ -157,7 +163,8 @@ int items_cap_for(const l4_decode_params* p, int64_t max_total_pages, int num_ct
   } else {
     // C >= T*Hkv/(W*k) => Hkv * sum ceil(p_b / C) <= W*k + Hkv*B
     cap = std::min(Hkv * (B + ceil_div64(max_total_pages, kMinChunk)),
-                   Hkv * B + (int64_t)num_ctas * kItemsPerCta + Hkv);
+                   Hkv * B + (int64_t)num_ctas * kItemsPerCta + Hkv) +
+          (int64_t)num_ctas * kTailChunksPerCta + (kTailChunksPerCta > 0 ? Hkv * B : 0);  // guided-tail splits
   }
   cap = std::max<int64_t>(cap, 1);
   return (int)std::min<int64_t>(cap, INT_MAX / 64);
@@ -255,12 +262,13 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
   // PDL: let the dependent decode kernel start its prologue now; it waits
   // (griddepcontrol.wait) for this grid's completion before reading the plan.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  extern __shared__ int plan_smem[];  // s_len[B], s_ptr[B], s_rb[B] (request at rank), s_off[B]
+  extern __shared__ int plan_smem[];  // s_len, s_ptr, s_rb (request at rank), s_off, s_ns (splits at rank)
   const int Bs = max(a.B, 1);
   int* s_len = plan_smem;
   int* s_ptr = plan_smem + Bs;
   int* s_rb = plan_smem + 2 * Bs;
   int* s_off = plan_smem + 3 * Bs;
+  int* s_ns = plan_smem + 4 * Bs;
   __shared__ long long s_ll[32];
   __shared__ int s_i[33];
   __shared__ unsigned s_u[32];
@@ -364,13 +372,63 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     if (tid < kNumBins) s_binbase[tid] += s_i[tid];
   }
   __syncthreads();
+  // ---- guided tail: the requests processed last (the suffix of the LPT order holding about
+  // kTailChunksPerCta chunks of C_tail pages per CTA) are split into C_tail-page chunks so that
+  // all CTAs finish within a small item of each other (auto mode only).
+  const bool auto_mode = a.forced_chunk == 0;
+  const long long per_cta = (T * a.Hkv + a.num_ctas - 1) / max(a.num_ctas, 1);
+  const int Ct = (int)max((long long)kMinTailChunk, min((long long)C, (per_cta + kTailDiv - 1) / kTailDiv));
+  const long long tail_budget = auto_mode ? (long long)kTailChunksPerCta * a.num_ctas * Ct : 0;
+  int tail_requests = 0;
+  {
+    long long carry = 0, extra = 0;
+    int ntail = 0;
+    for (int tile = 0; tile < a.B; tile += nthr) {  // exclusive prefix of page-heads in rank order
+      const int r = tile + tid;
+      const int pg = r < a.B ? pages_of(s_len[s_rb[r]]) : 0;
+      int tot;
+      const int ex = block_excl_scan(pg, &tot, s_i);
+      if (r < a.B) {
+        const long long suffix = (T - (carry + ex)) * a.Hkv;  // page-heads from rank r to the end
+        int ns = nsplit_of(pg, C);
+        if (suffix <= tail_budget && pg > 0) {
+          const int nt = min(nsplit_of(pg, Ct), kMaxSplits);
+          if (nt > ns) {
+            extra += (long long)(nt - ns) * a.Hkv;
+            ns = nt;
+          }
+          ntail += 1;
+        }
+        s_ns[r] = ns;
+      }
+      carry += tot;
+    }
+    long long ex_tot;
+    int ntail_tot;
+    unsigned unused2;
+    block_reduce3(extra, ntail, 0u, s_ll, s_i, s_u, &ex_tot, &ntail_tot, &unused2);
+    // block_reduce3's max is not a sum: count tail requests with a second pass
+    int cnt = 0;
+    for (int r = tid; r < a.B; r += nthr) cnt += s_ns[r] != nsplit_of(pages_of(s_len[s_rb[r]]), C) ? 1 : 0;
+    long long cnt_ll;
+    int dummy2;
+    block_reduce3(cnt, 0, 0u, s_ll, s_i, s_u, &cnt_ll, &dummy2, &unused2);
+    if (N + ex_tot > a.items_cap) {  // no room: keep the plain plan
+      for (int r = tid; r < a.B; r += nthr) s_ns[r] = nsplit_of(pages_of(s_len[s_rb[r]]), C);
+      ex_tot = 0;
+      cnt_ll = 0;
+    }
+    N += ex_tot;
+    tail_requests = (int)cnt_ll;
+  }
+  __syncthreads();
   // ---- item offsets: exclusive scan of nsplit * Hkv in rank order
   {
     int carry = 0;
     for (int tile = 0; tile < a.B; tile += nthr) {
       const int r = tile + tid;
       int cnt = 0;
-      if (r < a.B) cnt = nsplit_of(pages_of(s_len[s_rb[r]]), C) * a.Hkv;
+      if (r < a.B) cnt = s_ns[r] * a.Hkv;
       int tot;
       const int ex = block_excl_scan(cnt, &tot, s_i);
       if (r < a.B) s_off[r] = carry + ex;
@@ -384,7 +442,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     const int b = s_rb[r];
     const int L = s_len[b];
     const int pg = pages_of(L);
-    const int ns = nsplit_of(pg, C);
+    const int ns = s_ns[r];
     const int first = s_off[r] + h * ns;
     const int pbase = s_ptr[b];
     const int last_valid = pg > 0 ? L - (pg - 1) * kPage : 0;
@@ -405,6 +463,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     hd.chunk = C;
     hd.num_ctas = a.num_ctas;
     hd.max_splits = nsplit_of(Pmax, C);
+    hd.tail_requests = tail_requests;
+    hd.tail_chunk = tail_requests > 0 ? Ct : 0;
     hd.batch = a.B;
     hd.num_kv_heads = a.Hkv;
     hd.items_cap = a.items_cap;
@@ -995,10 +1055,10 @@ static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, con
   a.header = reinterpret_cast<PlanHeader*>(ws + L.header);
   a.items = reinterpret_cast<WorkItem*>(ws + L.items);
   a.counters = reinterpret_cast<int*>(ws + L.counters);
-  const size_t smem = (size_t)4 * std::max(p->batch, 1) * sizeof(int);
+  const size_t smem = (size_t)5 * std::max(p->batch, 1) * sizeof(int);
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kMaxBatch * (int)sizeof(int));
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * kMaxBatch * (int)sizeof(int));
     // same L1/shared carveout as decode_kernel: no SM reconfiguration between the two launches
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   });
@@ -1101,6 +1161,8 @@ extern "C" l4_status l4_decode_plan_info(const void* workspace, l4_plan_info* in
   info_out->chunk_pages = h.chunk;
   info_out->num_ctas = h.num_ctas;
   info_out->max_splits = h.max_splits;
+  info_out->tail_requests = h.tail_requests;
+  info_out->tail_chunk_pages = h.tail_chunk;
   return L4_OK;
 }
 

@@ -48,7 +48,8 @@ class DecodeParams(ctypes.Structure):
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [("num_items", ctypes.c_int32), ("chunk_pages", ctypes.c_int32), ("num_ctas", ctypes.c_int32),
-                ("max_splits", ctypes.c_int32)]
+                ("max_splits", ctypes.c_int32), ("tail_requests", ctypes.c_int32),
+                ("tail_chunk_pages", ctypes.c_int32)]
 
 
 class Stage(ctypes.Structure):

@@ -157,11 +157,14 @@ def test_plan_covers_every_token_once():
                 covered[key] = 1
             if pe == base + npg and L > 0:
                 assert last_valid == L - (npg - 1) * 16
-            # length bin of the item = bit_length of its request's largest split
-            sizes.append(0 if npg == 0 else -(-npg // ns))
-            # requests of <= 2C pages are never split
-            if npg <= 2 * info.chunk_pages:
-                assert ns == 1
+            # ordering key = bit_length of the request's largest split under the plain chunk C
+            C = info.chunk_pages
+            plain_ns = 1 if npg <= 2 * C else -(-npg // C)
+            sizes.append(0 if npg == 0 else -(-npg // plain_ns))
+            # requests of <= 2C pages are split only in the guided tail, into tail chunks
+            if ns != plain_ns:
+                Ct = info.tail_chunk_pages
+                assert chunk == 0 and Ct > 0 and ns == -(-npg // Ct) and ns > plain_ns
         expect = sum(8 * ((int(L) + 15) // 16) for L in table.kv_len)
         assert len(covered) == expect
         # length-binned, longest bin first: bins are non-increasing along the work list
