@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libl4.so")
+LIB_PATH = os.environ.get("L4_LIB") or os.path.join(_HERE, "libl4.so")  # L4_LIB: dev-only variant override
 
 L4_OK, L4_ERR_INVALID_ARG, L4_ERR_UNSUPPORTED, L4_ERR_CUDA, L4_ERR_WORKSPACE, L4_ERR_NO_PAGES, L4_ERR_INFEASIBLE = range(7)
 L4_DT_F32, L4_DT_BF16 = 0, 1
