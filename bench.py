@@ -386,7 +386,7 @@ def migration_bandwidth(reps: int = 5):
 
 
 # ----------------------------------------------------------------------------- pipeline (N > 1)
-def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, seed=0, shape=None):
+def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, seed=0, shape=None, precopy_lead=0):
     """C5: the length-aware pipeline on `world` GPUs.  Every step each rank runs the hot path
     (plan + split-KV kernel) on its resident batch, then the replicated control plane advances
     (tokens appended, handovers, retirements, arrivals) and KV pages of handed-over requests
@@ -396,7 +396,7 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
     import torch.distributed as dist
     from paper_2512_19179_b200 import l4, pipeline
     shape = shape or synth.SHAPE_LLAMA3_8B
-    sim = pipeline.ClusterSim(stages, concurrency=world * per_rank, seed=seed)
+    sim = pipeline.ClusterSim(stages, concurrency=world * per_rank, seed=seed, precopy_lead=precopy_lead)
     budget_pages = sim.token_budget // 16 * 5 // 4 + 2 * sim.batch_cap
     rt = pipeline.RankRuntime(sim, rank, budget_pages, shape, pipeline.DeviceOps(shape, device, seed + rank))
     cap = sim.batch_cap
@@ -450,6 +450,8 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
         tot["req_steps"] += B
     tot["elapsed_ms"] = t_start.elapsed_time(t_end)
     tot["launches"] = tot.get("launches", 0) + rt.stats["launches"]
+    for k_ in ("precopy_pages", "stop_pages", "single_pages"):
+        tot[k_] = rt.stats[k_]
     tot["fingerprint"] = sim.fingerprint()
     tot["stages"] = stages
     return tot
@@ -481,9 +483,12 @@ def pipeline_line(args, world, rank, local):
     torch.cuda.synchronize()
     dist.barrier()
     for name, st in (("l4", stages), ("round_robin", rr)):
-        t = run_pipeline_arm(st, args.steps, args.warmup, rank, world, device)
+        # L4 arm: live (two-round) migration with an 8-token pre-copy lead (NEXT#1)
+        t = run_pipeline_arm(st, args.steps, args.warmup, rank, world, device,
+                             precopy_lead=8 if name == "l4" else 0)
         vec = torch.tensor([t["kv_bytes"], t["tokens"], t["mig_bytes"], t["mig_count"], t["req_steps"],
-                            t["lat_ms_x_req"], t["launches"]], dtype=torch.float64, device=device)
+                            t["lat_ms_x_req"], t["launches"], t["precopy_pages"], t["stop_pages"],
+                            t["single_pages"]], dtype=torch.float64, device=device)
         dist.all_reduce(vec, op=dist.ReduceOp.SUM)
         tm = torch.tensor([t["elapsed_ms"], t["busy_ms"]], dtype=torch.float64, device=device)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -495,7 +500,8 @@ def pipeline_line(args, world, rank, local):
         res[name] = dict(kv_gbs=float(vec[0]) / (elapsed / 1e3) / 1e9, tokens_per_s=float(vec[1]) / (elapsed / 1e3),
                          elapsed_ms=elapsed, max_busy_ms=float(tm[1]), migrated_bytes=int(vec[2]),
                          migrations=int(vec[3]), mean_step_latency_ms=float(vec[5]) / max(1.0, float(vec[4])),
-                         launches=int(vec[6]),
+                         launches=int(vec[6]), precopy_pages=int(vec[7]), stop_round_pages=int(vec[8]),
+                         single_round_pages=int(vec[9]),
                          stages=[list(x) for x in st])
     if rank != 0:
         return None
@@ -543,10 +549,13 @@ def run_reference(args):
         vals.append(r["value"])
         samples = r
     v = float(np.mean(vals))
+    full_bytes = kv_bytes(spec["lens"](), spec["shape"])
+    ms_full = full_bytes / (v * 1e9) * 1e3          # the oracle's time for one whole step, at the sampled rate
     line = dict(impl="reference", metric=METRIC, value=round(v, 4), unit="GB/s", n_gpus=args.gpus,
-                steps=args.steps, warmup=args.warmup, ms_per_step=None, higher_is_better=True, scaling="weak",
-                vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=name, desc=spec["desc"], model=spec["shape"].name, global_batch=len(spec["lens"]())),
+                steps=args.steps, warmup=args.warmup, ms_per_step=round(ms_full, 3), higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=name, desc=spec["desc"], batch=len(spec["lens"]()),
+                            kv_bytes_per_step=full_bytes),
                 cpu_baseline=dict(value=round(v, 4), unit="GB/s", cores=samples["cores"], kind="oracle",
                                   sample=samples["sample"]),
                 e2e=dict(value=round(v, 4), unit="GB/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))

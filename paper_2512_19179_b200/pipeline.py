@@ -45,7 +45,11 @@ class Req:
 @dataclass
 class StepEvents:
     """What happened in one decode step, identical on every rank."""
-    migrations: List[Tuple[int, int, int, int]] = field(default_factory=list)  # (rid, src, dst, L at handover)
+    # handovers: (rid, src, dst, L at handover, first page to send); first page > 0 is the stop
+    # round of a live migration whose earlier pages were pre-copied (P:413)
+    migrations: List[Tuple[int, int, int, int, int]] = field(default_factory=list)
+    precopies: List[Tuple[int, int, int, int]] = field(default_factory=list)    # (rid, src, dst, pages)
+    cancelled: List[Tuple[int, int]] = field(default_factory=list)             # (rid, dst) live sessions dropped
     retired: List[Tuple[int, int]] = field(default_factory=list)               # (rid, rank)
     admitted: List[Tuple[int, int, int]] = field(default_factory=list)         # (rid, rank, L)
     deferred: int = 0                                                           # handovers over the cap
@@ -90,8 +94,14 @@ class ClusterSim:
     vectorised; only the few handovers / arrivals run Python loops."""
 
     def __init__(self, stages, concurrency: int, seed: int = 0, token_budget: int = 1_200_000,
-                 batch_cap: int = 1024, max_transfers: int = 3):
+                 batch_cap: int = 1024, max_transfers: int = 3, precopy_lead: int = 0):
         self.stages = [(int(lo), int(hi), int(m)) for lo, hi, m in stages]
+        # NEXT#1 live migration: a request within `precopy_lead` tokens of its stage's upper
+        # bound starts a session: its pages are pre-copied to the chosen receiver while it keeps
+        # decoding on the source; at the handover only the pages changed since are sent
+        # (stop round).  0 = single-round migration at the handover.
+        self.precopy_lead = int(precopy_lead)
+        self.sessions: Dict[int, list] = {}   # rid -> [src, dst, pages pre-copied]
         self.rank_stage = np.array(assign_ranks(self.stages), dtype=np.int64)
         self.n_ranks = len(self.rank_stage)
         self.stage_hi = np.array([hi for _, hi, _ in self.stages], dtype=np.int64)
@@ -180,27 +190,56 @@ class ClusterSim:
             self.tokens[r] -= self.L[i]
             self.count[r] -= 1
             self.active[i] = False
+        # 2b. live sessions of retired requests are dropped (the receiver frees its copy)
+        for rid, r in ev.retired:
+            ses = self.sessions.pop(rid, None)
+            if ses is not None:
+                ev.cancelled.append((rid, ses[1]))
         # 3. handover to the next stage when the length leaves the stage range
         act = self.active
         st = self.rank_stage[np.maximum(self.rank, 0)]
-        cand = np.nonzero(act & (st != self.last_stage) & (self.L >= self.stage_hi[st]))[0]
-        sent = np.zeros(self.n_ranks, dtype=np.int64)
+        nonlast = act & (st != self.last_stage)
+        hi = self.stage_hi[st]
+        cand = np.nonzero(nonlast & (self.L >= hi))[0]
+        inflight = np.zeros(self.n_ranks, dtype=np.int64)   # transfers in flight per sender
+        for ses in self.sessions.values():
+            inflight[ses[0]] += 1
         for i in cand:                       # slot order: deterministic on every rank
-            src, L = int(self.rank[i]), int(self.L[i])
-            if sent[src] >= self.max_transfers:        # keep running on the source
-                ev.deferred += 1
-                continue
-            dst = self.least_loaded(self.stage_of(L), L)
-            if dst is None:                            # no idle cache downstream: skip
-                ev.deferred += 1
-                continue
+            rid, src, L = int(self.rid[i]), int(self.rank[i]), int(self.L[i])
+            ses = self.sessions.pop(rid, None)
+            if ses is not None:                        # stop round of a live migration
+                dst, first = ses[1], max(ses[2] - 1, 0)
+                inflight[src] -= 1
+            else:
+                if inflight[src] >= self.max_transfers:    # keep running on the source
+                    ev.deferred += 1
+                    continue
+                dst = self.least_loaded(self.stage_of(L), L)
+                if dst is None:                            # no idle cache downstream: skip
+                    ev.deferred += 1
+                    continue
+                first = 0
+                inflight[src] += 1                          # single-round transfer this step
             self.tokens[src] -= L
             self.count[src] -= 1
             self.rank[i] = dst
             self.tokens[dst] += L
             self.count[dst] += 1
-            ev.migrations.append((int(self.rid[i]), src, dst, L))
-            sent[src] += 1
+            ev.migrations.append((rid, src, dst, L, first))
+        # 3b. live migration: start pre-copy rounds for requests about to leave their range
+        if self.precopy_lead > 0:
+            near = np.nonzero(nonlast & self.active & (self.L < hi) & (self.L >= hi - self.precopy_lead))[0]
+            for i in near:
+                rid, src, L = int(self.rid[i]), int(self.rank[i]), int(self.L[i])
+                if rid in self.sessions or inflight[src] >= self.max_transfers:
+                    continue
+                dst = self.least_loaded(self.stage_of(int(hi[i])), L + self.precopy_lead)
+                if dst is None:
+                    continue
+                npg = -(-L // PAGE)
+                self.sessions[rid] = [src, dst, npg]
+                inflight[src] += 1
+                ev.precopies.append((rid, src, dst, npg))
         # 4. arrivals: queued first, then one new request per retirement
         pending, self.queue = self.queue, []
         for _ in range(len(done)):
@@ -263,7 +302,9 @@ class RankRuntime:
         rids, Ls = sim.batch(rank)
         for rid, L in zip(rids.tolist(), Ls.tolist()):
             self._add(rid, ops.alloc(self.pool, -(-L // PAGE)))
-        self.stats = dict(migrated_pages=0, migrated_bytes=0, migrations_in=0, migrations_out=0, launches=0)
+        self.incoming: Dict[int, List[int]] = {}   # live migration: pages pre-copied to this rank
+        self.stats = dict(migrated_pages=0, migrated_bytes=0, migrations_in=0, migrations_out=0, launches=0,
+                          precopy_pages=0, stop_pages=0, single_pages=0)
 
     # ------------------------------------------------------------ page-table bookkeeping
     def _delta(self, slot, start, pages):
@@ -320,7 +361,7 @@ class RankRuntime:
                 self.ops.free(self.pool, self._drop(rid))
         # growth: the step's new token opens a new page when L-1 is a multiple of 16
         sim = self.sim
-        mig_out = {m[0] for m in ev.migrations if m[1] == me}
+        mig_out = {m[0] for m in ev.migrations if m[1] == me} | {p[0] for p in ev.precopies if p[1] == me}
         grow = np.nonzero(sim.active & ((sim.L - 1) % PAGE == 0))[0]
         for i in grow:
             rid = int(sim.rid[i])
@@ -328,25 +369,45 @@ class RankRuntime:
                 need = -(-int(sim.L[i]) // PAGE)
                 if need > len(self.pages[rid]):
                     self._append(rid, self.ops.alloc(self.pool, need - len(self.pages[rid])))
-        sends, recvs = [], []
-        for rid, src, dst, L in ev.migrations:
+        for rid, dst in ev.cancelled:                 # live session of a retired request
+            if dst == me and rid in self.incoming:
+                self.ops.free(self.pool, self.incoming.pop(rid))
+        # transfers in global event order: pre-copy rounds, then handovers (single or stop round)
+        sends, recvs, done_out, done_in = [], [], [], []
+        for rid, src, dst, npg in ev.precopies:
+            if src == me:
+                sends.append((dst, self.pages[rid][:npg]))
+                self.stats["precopy_pages"] += npg
+            elif dst == me:
+                pages = self.ops.alloc(self.pool, npg)
+                self.incoming[rid] = pages
+                recvs.append((src, pages))
+        for rid, src, dst, L, first in ev.migrations:
+            need = -(-L // PAGE)
             if src == me:
                 pages = self._drop(rid)
-                need = -(-L // PAGE)
                 if need > len(pages):
                     pages = pages + self.ops.alloc(self.pool, need - len(pages))
-                sends.append((rid, dst, pages))
+                sends.append((dst, pages[first:need]))
+                done_out.append(pages)
+                self.stats["stop_pages" if first > 0 else "single_pages"] += need - first
             elif dst == me:
-                recvs.append((rid, src, -(-L // PAGE)))
-        received: Dict[int, List[int]] = {}
-        nbytes = self.ops.transfer(self.pool, sends, recvs, comm, received)
-        for rid, pages in received.items():
+                have = self.incoming.pop(rid, [])[:first + 1] if first > 0 else []
+                if first > 0:
+                    pages = have[:first] + (have[first:first + 1] or self.ops.alloc(self.pool, 1))
+                else:
+                    pages = []
+                pages = pages + self.ops.alloc(self.pool, need - len(pages))
+                recvs.append((src, pages[first:need]))
+                done_in.append((rid, pages))
+        nbytes = self.ops.transfer(self.pool, sends, recvs, comm)
+        for rid, pages in done_in:
             self._add(rid, pages)
-        for rid, dst, pages in sends:
+        for pages in done_out:
             self.ops.free(self.pool, pages)
             self.stats["migrations_out"] += 1
             self.stats["migrated_pages"] += len(pages)
-        self.stats["migrations_in"] += len(recvs)
+        self.stats["migrations_in"] += len(done_in)
         self.stats["migrated_bytes"] += nbytes
         self.stats["launches"] += len(sends) + len(recvs)
         for rid, r, L in ev.admitted:
@@ -392,28 +453,29 @@ class DeviceOps:
         v = torch.from_numpy(val).pin_memory().to(self.device, non_blocking=True)
         table.index_copy_(0, p, v)
 
-    def transfer(self, pool, sends, recvs, comm, page_map):
-        """Pack outgoing pages, exchange with batched NCCL P2P, unpack into newly allocated
-        idle pages.  Returns bytes moved by this rank (sent + received)."""
+    def transfer(self, pool, sends, recvs, comm):
+        """sends = [(dst rank, src page ids)], recvs = [(src rank, dst page ids)] in the global
+        event order: pack -> batched NCCL P2P -> unpack straight into the receiver's pages
+        (allocated by the caller in idle slots).  Returns bytes moved by this rank."""
         torch, l4, dist = self.torch, self.l4, comm
         if not sends and not recvs:
             return 0
         pb = pool["view"].page_bytes
         ops, bufs, nbytes = [], [], 0
-        for rid, dst, pages in sends:
-            st = torch.empty(len(pages) * 2 * pb, dtype=torch.uint8, device=self.device)
-            l4.pack_pages(pool["view"], pages, st)
+        for dst, pages in sends:
+            st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device=self.device)
+            if pages:
+                l4.pack_pages(pool["view"], pages, st)
             ops.append(dist.P2POp(dist.isend, st, dst))
-            nbytes += st.numel()
-        for rid, src, npages in recvs:
-            st = torch.empty(npages * 2 * pb, dtype=torch.uint8, device=self.device)
+            nbytes += len(pages) * 2 * pb
+        for src, pages in recvs:
+            st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device=self.device)
             ops.append(dist.P2POp(dist.irecv, st, src))
-            bufs.append((rid, npages, st))
-            nbytes += st.numel()
+            bufs.append((pages, st))
+            nbytes += len(pages) * 2 * pb
         for w in dist.batch_isend_irecv(ops):
             w.wait()
-        for rid, npages, st in bufs:
-            pages = self.alloc(pool, npages)
-            l4.unpack_pages(pool["view"], pages, st)
-            page_map[rid] = pages
+        for pages, st in bufs:
+            if pages:
+                l4.unpack_pages(pool["view"], pages, st)
         return nbytes

@@ -34,10 +34,10 @@ def test_sim_deterministic_and_conserving():
         ea, eb = a.step(), b.step()
         assert ea.migrations == eb.migrations and ea.retired == eb.retired and ea.admitted == eb.admitted
         # handovers go to the next stage, capped at 3 per sender
-        for rid, src, dst, L in ea.migrations:
+        for rid, src, dst, L, first in ea.migrations:
             assert a.rank_stage[dst] == a.rank_stage[src] + 1 or a.rank_stage[dst] > a.rank_stage[src]
         per_src = {}
-        for _, src, _, _ in ea.migrations:
+        for _, src, _, _, _ in ea.migrations:
             per_src[src] = per_src.get(src, 0) + 1
         assert all(v <= 3 for v in per_src.values())
         # tokens bookkeeping equals the sum of resident lengths
@@ -64,36 +64,35 @@ class MockOps:
     def free(self, pool, pages):
         pool["alloc"].free(pages)
 
-    def transfer(self, pool, sends, recvs, comm, page_map):
+    def transfer(self, pool, sends, recvs, comm):
         ops, bufs, nbytes = [], [], 0
-        for rid, dst, pages in sends:
+        for dst, pages in sends:
             idx = torch.tensor(pages, dtype=torch.long)
             st = torch.cat([pool["k"][idx], pool["v"][idx]], dim=1).contiguous()
             ops.append(dist.P2POp(dist.isend, st, dst))
             nbytes += st.numel() * 4
-        for rid, src, npages in recvs:
-            st = torch.empty(npages, 2 * self.page_elems)
+        for src, pages in recvs:
+            st = torch.empty(len(pages), 2 * self.page_elems)
             ops.append(dist.P2POp(dist.irecv, st, src))
-            bufs.append((rid, npages, st))
+            bufs.append((pages, st))
             nbytes += st.numel() * 4
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        for rid, npages, st in bufs:
-            pages = self.alloc(pool, npages)
+        for pages, st in bufs:
             idx = torch.tensor(pages, dtype=torch.long)
             pool["k"][idx] = st[:, :self.page_elems]
             pool["v"][idx] = st[:, self.page_elems:]
-            page_map[rid] = pages
         return nbytes
 
 
-def _worker(rank, world, port, stages, steps, out_q):
+def _worker(rank, world, port, stages, steps, out_q, lead=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        sim = pipeline.ClusterSim(stages, concurrency=48 * world, seed=5, token_budget=400_000, batch_cap=256)
+        sim = pipeline.ClusterSim(stages, concurrency=48 * world, seed=5, token_budget=400_000, batch_cap=256,
+                                  precopy_lead=lead)
         ops = MockOps()
         rt = pipeline.RankRuntime(sim, rank, num_pages=400_000 // 16 * 2, shape=None, ops=ops)
         pool = rt.pool
@@ -122,7 +121,7 @@ def _worker(rank, world, port, stages, steps, out_q):
             assert set(rids.tolist()) == set(rt.pages)
             for rid, L in zip(rids.tolist(), Ls.tolist()):
                 assert len(rt.pages[rid]) == -(-L // 16)
-            used = sum(len(p) for p in rt.pages.values())
+            used = sum(len(p) for p in rt.pages.values()) + sum(len(p) for p in rt.incoming.values())
             assert pool["alloc"].num_free() == pool["alloc"].num_pages - used
         fps = [None] * world
         dist.all_gather_object(fps, sim.fingerprint())
@@ -139,13 +138,13 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_pipeline_gloo_migrations(world):
+@pytest.mark.parametrize("world,lead", [(2, 0), (3, 0), (2, 6), (3, 3)])
+def test_pipeline_gloo_migrations(world, lead):
     stages = [(0, 1500, 1), (1500, 262144, world - 1)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, stages, 120, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, stages, 120, q, lead)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -158,3 +157,9 @@ def test_pipeline_gloo_migrations(world):
     outs = sum(s["migrations_out"] for *_, s in res)
     ins = sum(s["migrations_in"] for *_, s in res)
     assert outs == ins == total_checked
+    stop = sum(s["stop_pages"] for *_, s in res)
+    pre = sum(s["precopy_pages"] for *_, s in res)
+    if lead > 0:   # live migration: most pages move in the pre-copy round, the stop round is small
+        assert pre > 0 and stop > 0 and stop < pre
+    else:
+        assert pre == 0 and stop == 0

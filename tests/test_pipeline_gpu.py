@@ -69,14 +69,15 @@ def _attention_check(rt, shape, q):
     return B
 
 
-def test_two_instances_loopback_migration():
+@pytest.mark.parametrize("lead", [0, 4])
+def test_two_instances_loopback_migration(lead):
     shape = synth.AttnShape("t", 8, 2)
     # put the stage boundary just above the median resident length so handovers happen soon
     probe = pipeline.ClusterSim([(0, 1 << 21, 2)], concurrency=40, seed=2, token_budget=10 ** 9, batch_cap=128)
     Ls = sorted(q.L for q in probe.reqs.values())
     cut = Ls[len(Ls) // 2] + 8
     stages = [(0, cut, 1), (cut, 1 << 21, 1)]
-    sim = pipeline.ClusterSim(stages, concurrency=40, seed=2, token_budget=10 ** 9, batch_cap=128)
+    sim = pipeline.ClusterSim(stages, concurrency=40, seed=2, token_budget=10 ** 9, batch_cap=128, precopy_lead=lead)
     ops = pipeline.DeviceOps(shape, "cuda", seed=1)
     rts = [pipeline.RankRuntime(sim, r, 60000, shape, ops) for r in range(2)]
     hub = _Hub()
@@ -87,10 +88,22 @@ def test_two_instances_loopback_migration():
             for rt in rts:
                 _attention_check(rt, shape, q)
         ev = sim.step()
+        # the token each request produced this step is appended on its current owner before any
+        # handover: write it into the owner's partial page (a stale pre-copied page then shows)
+        for rt in rts:
+            for rid, pages in rt.pages.items():
+                L = sim.reqs[rid].L if rid in sim.reqs else None
+                if L is None:
+                    continue
+                pidx, slot = (L - 1) // 16, (L - 1) % 16
+                if pidx < len(pages):
+                    val = float((rid * 7 + L) % 251) / 8.0
+                    rt.pool["k"][pages[pidx], :, slot, :] = val
+                    rt.pool["v"][pages[pidx], :, slot, :] = -val
         # snapshot the source pages of migrating requests (after this step's growth allocation
         # the source packs exactly these pages plus possibly one new page)
         snaps = {}
-        for rid, src, dst, L in ev.migrations:
+        for rid, src, dst, L, first in ev.migrations:
             pages = list(rts[src].pages[rid])
             snaps[rid] = (rts[src].pool["k"][torch.tensor(pages, device="cuda")].clone(),
                           rts[src].pool["v"][torch.tensor(pages, device="cuda")].clone(), len(pages))
@@ -98,7 +111,7 @@ def test_two_instances_loopback_migration():
             hub.me = r
             rts[r].apply(ev, hub)
         torch.cuda.synchronize()
-        for rid, src, dst, L in ev.migrations:
+        for rid, src, dst, L, first in ev.migrations:
             k0, v0, n0 = snaps[rid]
             pages = rts[dst].pages[rid]
             assert len(pages) == -(-L // 16)
