@@ -320,6 +320,20 @@ def mixed_vs_binned(steps: int, warmup: int):
         del w
     res["c3_binned_same_requests"] = dict(gbs=round(b_sum / (t_sum / 1e3) / 1e9, 1), ms=round(t_sum, 4), bins=bins)
     torch.cuda.empty_cache()
+    # (iii) stage-shaped binned: for each length class a homogeneous batch (the class's median
+    # length) refilled to about the C3 KV volume (<= 1024 requests): what an L4 stage instance sees
+    stage_shaped = []
+    for b in bins:
+        sel = lens[(lens >= b["lo"]) & (lens < (b["hi"] or (1 << 30)))]
+        L = int(np.median(sel))
+        n = int(min(1024, max(1, round(lens.sum() / L))))
+        w = Workload(f"stage[{b['lo']}]", np.full(n, L, dtype=np.int64), shape)
+        t, _, _ = time_steps(w, steps, warmup)
+        stage_shaped.append(dict(lo=b["lo"], hi=b["hi"], length=L, batch=n,
+                                 gbs=round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1)))
+        del w
+        torch.cuda.empty_cache()
+    res["c3_stage_shaped_binned"] = stage_shaped
     w = Workload("c4", synth.lengths_c4(0), synth.SHAPE_LLAMA3_70B)
     t, _, info = time_steps(w, steps, warmup)
     res["c4"] = dict(gbs=round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1), ms=round(t / steps, 4),
@@ -667,6 +681,8 @@ def main():
                      "traffic_source": traffic_src,
                      "peak_source": peak_src, "launch_ms": round(run_avg, 5),
                      "bytes_per_launch": wl.bytes_algo},
+        "amortized_32_layers": {"note": "one plan per decode iteration reused by 32 layers: plan + 32 x run",
+                                "gbs": round(32 * wl.bytes_kv / ((ms_step - run_avg + 32 * run_avg) / 1e3) / 1e9, 1)},
         "e2e": {"value": round(ws * wl.bytes_kv / (e2e_step / 1e3) / 1e9, 1), "unit": "GB/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_step, 5)},
         "gpu_launches": 2 * args.steps,

@@ -51,33 +51,33 @@ __device__ __forceinline__ char* slice_addr(const Side& s, int page, long long p
   return s.k + (((pair_index * layers) + layer) * 2 + kv) * page_bytes;
 }
 
+// One CTA iteration copies one whole (page, layer, K|V) slice: the slice index is decoded once,
+// then every thread moves kUnroll 16-byte chunks with all loads issued before the stores.
+constexpr int kUnroll = 8;
 __global__ void __launch_bounds__(kCopyThreads) copy_pages_kernel(const __grid_constant__ CopyArgs a) {
   const long long chunks = a.page_bytes >> 4;  // 16-byte units per slice
   const long long slices = (long long)a.n * a.layers * 2;
-  const long long total = slices * chunks;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += stride * 4) {
-    int4 v[4];
-    char* dptr[4];
+  for (long long sl = blockIdx.x; sl < slices; sl += gridDim.x) {
+    const int kv = (int)(sl & 1);
+    const long long pl = sl >> 1;
+    const int layer = (int)(pl % a.layers);
+    const int i = (int)(pl / a.layers);
+    const int4* src = reinterpret_cast<const int4*>(
+        slice_addr(a.src, a.src_page[i], a.stage_base + i, layer, kv, a.page_bytes, a.layers));
+    int4* dst = reinterpret_cast<int4*>(slice_addr(a.dst, a.dst_page[i], a.stage_base + i, layer, kv, a.page_bytes, a.layers));
+    for (long long c0 = threadIdx.x; c0 < chunks; c0 += (long long)kCopyThreads * kUnroll) {
+      int4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const long long x = base + u * stride;
-      dptr[u] = nullptr;
-      if (x < total) {
-        const long long sl = x / chunks, ch = x - sl * chunks;
-        const int kv = (int)(sl & 1);
-        const long long pl = sl >> 1;
-        const int layer = (int)(pl % a.layers);
-        const int i = (int)(pl / a.layers);
-        const char* s = slice_addr(a.src, a.src_page[i], a.stage_base + i, layer, kv, a.page_bytes, a.layers);
-        char* d = slice_addr(a.dst, a.dst_page[i], a.stage_base + i, layer, kv, a.page_bytes, a.layers);
-        v[u] = __ldcs(reinterpret_cast<const int4*>(s) + ch);
-        dptr[u] = d + ch * 16;
+      for (int u = 0; u < kUnroll; ++u) {
+        const long long c = c0 + (long long)u * kCopyThreads;
+        if (c < chunks) v[u] = __ldcs(src + c);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const long long c = c0 + (long long)u * kCopyThreads;
+        if (c < chunks) __stcs(dst + c, v[u]);
       }
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (dptr[u]) __stcs(reinterpret_cast<int4*>(dptr[u]), v[u]);
   }
 }
 
@@ -107,17 +107,15 @@ l4_status check_pages(const int32_t* pages, int64_t n, int64_t num_pages, const 
   return L4_OK;
 }
 
-int copy_grid(long long total_chunks) {
+int copy_grid(long long slices) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long want = (total_chunks + (long long)kCopyThreads * 4 - 1) / ((long long)kCopyThreads * 4);
-  return (int)std::max<long long>(1, std::min<long long>(want, 2LL * sms));
+  return (int)std::max<long long>(1, std::min<long long>(slices, 2LL * sms));  // <= 2 CTAs per SM
 }
 
 l4_status launch_copies(const Side& src, const Side& dst, long long page_bytes, int layers, const int32_t* sp,
                         const int32_t* dp, int64_t n, cudaStream_t st) {
-  std::vector<CopyArgs> chunks;
   for (int64_t off = 0; off < n; off += kPairsPerLaunch) {
     CopyArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -131,8 +129,7 @@ l4_status launch_copies(const Side& src, const Side& dst, long long page_bytes, 
       a.src_page[i] = sp ? sp[off + i] : 0;
       a.dst_page[i] = dp ? dp[off + i] : 0;
     }
-    const long long total = (long long)a.n * layers * 2 * (page_bytes >> 4);
-    copy_pages_kernel<<<copy_grid(total), kCopyThreads, 0, st>>>(a);
+    copy_pages_kernel<<<copy_grid((long long)a.n * layers * 2), kCopyThreads, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       set_error("copy_pages_kernel launch failed: %s", cudaGetErrorString(e));
