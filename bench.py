@@ -400,7 +400,8 @@ def migration_bandwidth(reps: int = 5):
 
 
 # ----------------------------------------------------------------------------- pipeline (N > 1)
-def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, seed=0, shape=None, precopy_lead=0):
+def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, seed=0, shape=None, precopy_lead=0,
+                     policy="least_loaded", rebalance_every=0):
     """C5: the length-aware pipeline on `world` GPUs.  Every step each rank runs the hot path
     (plan + split-KV kernel) on its resident batch, then the replicated control plane advances
     (tokens appended, handovers, retirements, arrivals) and KV pages of handed-over requests
@@ -410,7 +411,8 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
     import torch.distributed as dist
     from paper_2512_19179_b200 import l4, pipeline
     shape = shape or synth.SHAPE_LLAMA3_8B
-    sim = pipeline.ClusterSim(stages, concurrency=world * per_rank, seed=seed, precopy_lead=precopy_lead)
+    sim = pipeline.ClusterSim(stages, concurrency=world * per_rank, seed=seed, precopy_lead=precopy_lead,
+                              policy=policy, rebalance_every=rebalance_every)
     budget_pages = sim.token_budget // 16 * 5 // 4 + 2 * sim.batch_cap
     rt = pipeline.RankRuntime(sim, rank, budget_pages, shape, pipeline.DeviceOps(shape, device, seed + rank))
     cap = sim.batch_cap
@@ -467,6 +469,7 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
     for k_ in ("precopy_pages", "stop_pages", "single_pages"):
         tot[k_] = rt.stats[k_]
     tot["fingerprint"] = sim.fingerprint()
+    tot["stage_cv"] = sim.stage_cv()
     tot["stages"] = stages
     return tot
 
@@ -497,9 +500,13 @@ def pipeline_line(args, world, rank, local):
     torch.cuda.synchronize()
     dist.barrier()
     for name, st in (("l4", stages), ("round_robin", rr)):
-        # L4 arm: live (two-round) migration with an 8-token pre-copy lead (NEXT#1)
+        # L4 arm: bid-ask receivers + intra-stage rebalancing and live (two-round)
+        # migration with an 8-token pre-copy lead; baseline: one length-agnostic stage,
+        # round-robin placement
+        l4arm = name == "l4"
         t = run_pipeline_arm(st, args.steps, args.warmup, rank, world, device,
-                             precopy_lead=8 if name == "l4" else 0)
+                             precopy_lead=8 if l4arm else 0, policy="bidask" if l4arm else "round_robin",
+                             rebalance_every=10 if l4arm else 0)
         vec = torch.tensor([t["kv_bytes"], t["tokens"], t["mig_bytes"], t["mig_count"], t["req_steps"],
                             t["lat_ms_x_req"], t["launches"], t["precopy_pages"], t["stop_pages"],
                             t["single_pages"]], dtype=torch.float64, device=device)
@@ -514,6 +521,7 @@ def pipeline_line(args, world, rank, local):
         res[name] = dict(kv_gbs=float(vec[0]) / (elapsed / 1e3) / 1e9, tokens_per_s=float(vec[1]) / (elapsed / 1e3),
                          elapsed_ms=elapsed, max_busy_ms=float(tm[1]), migrated_bytes=int(vec[2]),
                          migrations=int(vec[3]), mean_step_latency_ms=float(vec[5]) / max(1.0, float(vec[4])),
+                         stage_cv=[round(x, 4) for x in t["stage_cv"]],
                          launches=int(vec[6]), precopy_pages=int(vec[7]), stop_round_pages=int(vec[8]),
                          single_round_pages=int(vec[9]),
                          stages=[list(x) for x in st])

@@ -55,6 +55,24 @@ class StepEvents:
     deferred: int = 0                                                           # handovers over the cap
 
 
+def detect_overload(my_load: float, stage_loads, factor: float = 1.25) -> bool:
+    """an instance is an overloaded outlier when its request-memory demand is more
+    than 25% above the stage average (strict, S:399 decision)."""
+    loads = list(stage_loads)
+    return len(loads) > 0 and my_load > factor * (sum(loads) / len(loads))
+
+
+def select_receiver(bids):
+    """P:395-399 bid-ask: bids = [(receiver, load, earliest_start, reply_time)].  Keep the
+    lower-load half (ceil(k/2)), then the three earliest transmission starts, then the one that
+    replied first; ties by receiver id at every step."""
+    if not bids:
+        return None
+    half = sorted(bids, key=lambda b: (b[1], b[0]))[: (len(bids) + 1) // 2]
+    early = sorted(half, key=lambda b: (b[2], b[0]))[:3]
+    return min(early, key=lambda b: (b[3], b[0]))[0]
+
+
 def assign_ranks(stages) -> List[int]:
     """rank -> stage index: stage k takes the next instances_k ranks (NVSwitch: placement is free)."""
     out = []
@@ -94,8 +112,20 @@ class ClusterSim:
     vectorised; only the few handovers / arrivals run Python loops."""
 
     def __init__(self, stages, concurrency: int, seed: int = 0, token_budget: int = 1_200_000,
-                 batch_cap: int = 1024, max_transfers: int = 3, precopy_lead: int = 0):
+                 batch_cap: int = 1024, max_transfers: int = 3, precopy_lead: int = 0,
+                 policy: str = "least_loaded", rebalance_every: int = 0, overload_factor: float = 1.25,
+                 migrate_Bps: float = 7.7e11, kv_bytes_per_token: int = 131072):
         self.stages = [(int(lo), int(hi), int(m)) for lo, hi, m in stages]
+        # receiver choice within a stage: "least_loaded", "bidask" (P:395-399) or "round_robin";
+        # intra-stage rebalancing of overloaded instances every `rebalance_every` steps (P:391-393)
+        assert policy in ("least_loaded", "bidask", "round_robin")
+        self.policy = policy
+        self.rebalance_every = int(rebalance_every)
+        self.overload_factor = float(overload_factor)
+        self.migrate_Bps, self.kvb = float(migrate_Bps), int(kv_bytes_per_token)
+        self.step_no = 0
+        self.queued_tokens = None         # per-rank tokens being handed to it this step (earliest start)
+        self._rr = {}
         # NEXT#1 live migration: a request within `precopy_lead` tokens of its stage's upper
         # bound starts a session: its pages are pre-copied to the chosen receiver while it keeps
         # decoding on the source; at the handover only the pages changed since are sent
@@ -142,11 +172,33 @@ class ClusterSim:
                 return k
         return self.last_stage
 
-    def least_loaded(self, stage: int, extra_tokens: int = 0):
+    def _fits(self, r: int, extra_tokens: int) -> bool:
+        return self.count[r] < self.batch_cap and self.tokens[r] + extra_tokens <= self.token_budget
+
+    def least_loaded(self, stage: int, extra_tokens: int = 0, exclude: int = -1):
+        """Receiver of a request in `stage` under the configured policy; instances without
+        idle KV capacity abstain."""
+        cands = [r for r in self.stage_ranks[stage] if r != exclude and self._fits(r, extra_tokens)]
+        if not cands:
+            return None
+        if self.policy == "round_robin":
+            k = self._rr.get(stage, 0)
+            order = self.stage_ranks[stage]
+            for t in range(len(order)):
+                r = order[(k + t) % len(order)]
+                if r in cands:
+                    self._rr[stage] = (k + t + 1) % len(order)
+                    return r
+        if self.policy == "bidask":
+            q = self.queued_tokens
+            bids = []
+            for r in cands:
+                start = (0.0 if q is None else float(q[r])) * self.kvb / self.migrate_Bps   # earliest start (s)
+                reply = ((self.step_no * 1000003 + r * 7919 + extra_tokens * 31) % 1009) / 1009.0  # deterministic
+                bids.append((r, int(self.tokens[r]), start, reply))
+            return select_receiver(bids)
         best = None
-        for r in self.stage_ranks[stage]:
-            if self.count[r] >= self.batch_cap or self.tokens[r] + extra_tokens > self.token_budget:
-                continue
+        for r in cands:
             if best is None or self.tokens[r] < self.tokens[best]:
                 best = r
         return best
@@ -178,6 +230,8 @@ class ClusterSim:
     # ---------------------------------------------------------------- one decode step
     def step(self) -> StepEvents:
         ev = StepEvents()
+        self.step_no += 1
+        self.queued_tokens = np.zeros(self.n_ranks, dtype=np.int64)
         act = self.active
         # 1. every resident request generated one token: its KV grows by one
         self.L[act] += 1
@@ -220,11 +274,7 @@ class ClusterSim:
                     continue
                 first = 0
                 inflight[src] += 1                          # single-round transfer this step
-            self.tokens[src] -= L
-            self.count[src] -= 1
-            self.rank[i] = dst
-            self.tokens[dst] += L
-            self.count[dst] += 1
+            self._move(i, src, dst, L)
             ev.migrations.append((rid, src, dst, L, first))
         # 3b. live migration: start pre-copy rounds for requests about to leave their range
         if self.precopy_lead > 0:
@@ -240,6 +290,9 @@ class ClusterSim:
                 self.sessions[rid] = [src, dst, npg]
                 inflight[src] += 1
                 ev.precopies.append((rid, src, dst, npg))
+        # 3c. intra-stage rebalancing of overloaded instances via bid-ask
+        if self.rebalance_every > 0 and self.step_no % self.rebalance_every == 0:
+            self._rebalance(ev, inflight)
         # 4. arrivals: queued first, then one new request per retirement
         pending, self.queue = self.queue, []
         for _ in range(len(done)):
@@ -249,6 +302,51 @@ class ClusterSim:
             if r is not None:
                 ev.admitted.append((rid, r, I))
         return ev
+
+    def _move(self, i, src, dst, L):
+        self.tokens[src] -= L
+        self.count[src] -= 1
+        self.rank[i] = dst
+        self.tokens[dst] += L
+        self.count[dst] += 1
+        self.queued_tokens[dst] += L
+
+    def _rebalance(self, ev, inflight):
+        """An instance whose load exceeds 1.25x its stage mean hands requests (largest first,
+        slot order on ties) to bid-ask winners among its stage peers until it is no longer an
+        outlier or its transfer cap is reached."""
+        for k, ranks in enumerate(self.stage_ranks):
+            if len(ranks) < 2:
+                continue
+            for src in ranks:
+                loads = [int(self.tokens[r]) for r in ranks]
+                if not detect_overload(int(self.tokens[src]), loads, self.overload_factor):
+                    continue
+                mine = np.nonzero(self.active & (self.rank == src))[0]
+                mine = sorted(mine.tolist(), key=lambda i: (-int(self.L[i]), i))
+                mean = sum(loads) / len(loads)
+                for i in mine:
+                    if inflight[src] >= self.max_transfers or self.tokens[src] <= mean:
+                        break
+                    rid, L = int(self.rid[i]), int(self.L[i])
+                    if rid in self.sessions:
+                        continue
+                    dst = self.least_loaded(k, L, exclude=src)
+                    if dst is None or self.tokens[dst] + L >= self.tokens[src]:
+                        continue                    # would not reduce the imbalance
+                    self._move(i, src, dst, L)
+                    inflight[src] += 1
+                    ev.migrations.append((rid, src, dst, L, 0))
+
+    def stage_cv(self):
+        """Per-stage coefficient of variation of resident tokens (Fig. 16 metric)."""
+        out = []
+        for ranks in self.stage_ranks:
+            if len(ranks) < 2:
+                continue
+            x = np.array([self.tokens[r] for r in ranks], dtype=np.float64)
+            out.append(float(x.std() / x.mean()) if x.mean() > 0 else 0.0)
+        return out
 
     def batch(self, rank: int):
         """Resident requests of a rank in slot order: (rid array, L array)."""

@@ -163,3 +163,48 @@ def test_pipeline_gloo_migrations(world, lead):
         assert pre > 0 and stop > 0 and stop < pre
     else:
         assert pre == 0 and stop == 0
+
+
+def test_detect_overload_examples():
+    """strictly more than 25% above the stage mean."""
+    assert not pipeline.detect_overload(100, [100, 100, 100, 100])
+    assert pipeline.detect_overload(200, [100, 100, 100, 200])          # 200 > 1.25 * 125
+    assert not pipeline.detect_overload(150, [100, 100, 150, 150])      # 150 < 1.25 * 125
+    assert not pipeline.detect_overload(1.25 * 100, [100, 100, 100, 100], 1.25)   # boundary: not overloaded
+
+
+def test_select_receiver_examples_and_properties():
+    """lower-load half -> 3 earliest starts -> first reply, ties by id."""
+    assert pipeline.select_receiver([(7, 5, 0.0, 0.0)]) == 7
+    assert pipeline.select_receiver([(0, 10, 0, 0), (1, 20, 0, 0), (2, 30, 0, 0), (3, 40, 0, 0)]) == 0
+    assert pipeline.select_receiver([]) is None
+    rng = np.random.default_rng(0)
+    for _ in range(2000):
+        k = int(rng.integers(1, 12))
+        bids = [(r, int(rng.integers(0, 50)), float(rng.integers(0, 5)), float(rng.random())) for r in range(k)]
+        w = pipeline.select_receiver(bids)
+        half = sorted(bids, key=lambda b: (b[1], b[0]))[: (k + 1) // 2]
+        assert w in [b[0] for b in half]                                    # lower-load half
+        early = sorted(half, key=lambda b: (b[2], b[0]))[:3]
+        assert w in [b[0] for b in early]                                   # three earliest starts
+        assert min(early, key=lambda b: (b[3], b[0]))[0] == w               # first reply
+
+
+def test_bidask_balances_stages_fig16():
+    """Fig. 16 (`fig:load-balancing`) analogue, 4 stages x 4 instances: per-stage CV of
+    resident tokens with full bid-ask < bid-ask on handovers only < round-robin."""
+    stages = [(0, 1024, 4), (1024, 4096, 4), (4096, 16384, 4), (16384, 262144, 4)]
+    res = {}
+    for name, pol, reb in (("rr", "round_robin", 0), ("inter", "bidask", 0), ("full", "bidask", 5)):
+        cvs = []
+        for seed in range(2):
+            sim = pipeline.ClusterSim(stages, 16 * 16, seed=seed, policy=pol, rebalance_every=reb,
+                                      token_budget=2_000_000)
+            for s in range(500):
+                ev = sim.step()
+                for rid, src, dst, L, first in ev.migrations:       # rebalancing stays inside a stage
+                    assert sim.rank_stage[dst] >= sim.rank_stage[src]
+                if s >= 100 and s % 10 == 0:
+                    cvs.append(np.mean(sim.stage_cv()))
+        res[name] = float(np.mean(cvs))
+    assert res["full"] < res["inter"] < res["rr"], res
