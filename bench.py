@@ -479,21 +479,19 @@ def pipeline_line(args, world, rank, local):
     import torch.distributed as dist
     from paper_2512_19179_b200 import pipeline
     device = torch.device("cuda", local)
+    cdev = device if dist.get_backend() == "nccl" else torch.device("cpu")   # collectives' device
     peak, peak_src = load_peaks()
     stages, obj = pipeline.plan_stages(world, seed=0)
     rr = [(0, stages[-1][1], world)]                       # length-agnostic: one stage of all instances
     res = {}
     dist.barrier()                                          # first collective on the group
-    # warm up the NCCL P2P connections between adjacent stages outside the timed region
-    rank_stage = pipeline.assign_ranks(stages)
+    # warm up the NCCL P2P connections between every pair of ranks (handovers go to the next
+    # stage, rebalancing stays inside a stage) outside the timed region
     ops = []
-    for s_ in range(world):
-        for d_ in range(world):
-            if rank_stage[d_] == rank_stage[s_] + 1:
-                if rank == s_:
-                    ops.append(dist.P2POp(dist.isend, torch.ones(1, device=device), d_))
-                if rank == d_:
-                    ops.append(dist.P2POp(dist.irecv, torch.empty(1, device=device), s_))
+    for peer in range(world):
+        if peer != rank:
+            ops.append(dist.P2POp(dist.isend, torch.ones(1, device=cdev), peer))
+            ops.append(dist.P2POp(dist.irecv, torch.empty(1, device=cdev), peer))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
@@ -509,11 +507,11 @@ def pipeline_line(args, world, rank, local):
                              rebalance_every=10 if l4arm else 0)
         vec = torch.tensor([t["kv_bytes"], t["tokens"], t["mig_bytes"], t["mig_count"], t["req_steps"],
                             t["lat_ms_x_req"], t["launches"], t["precopy_pages"], t["stop_pages"],
-                            t["single_pages"]], dtype=torch.float64, device=device)
+                            t["single_pages"]], dtype=torch.float64, device=cdev)
         dist.all_reduce(vec, op=dist.ReduceOp.SUM)
-        tm = torch.tensor([t["elapsed_ms"], t["busy_ms"]], dtype=torch.float64, device=device)
+        tm = torch.tensor([t["elapsed_ms"], t["busy_ms"]], dtype=torch.float64, device=cdev)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        fp = torch.tensor([t["fingerprint"] & 0x7FFFFFFF], dtype=torch.int64, device=device)
+        fp = torch.tensor([t["fingerprint"] & 0x7FFFFFFF], dtype=torch.int64, device=cdev)
         fps = [torch.zeros_like(fp) for _ in range(world)]
         dist.all_gather(fps, fp)
         assert all(int(x) == int(fp) for x in fps), "replicated control plane diverged"
@@ -604,10 +602,17 @@ def main():
 
     import torch
     ws, rank, local = dist_env()
+    # development only: L4_FORCE_DEVICE pins every rank to one GPU and L4_PIPE_BACKEND=gloo
+    # swaps NCCL for gloo (host-staged transport), so the N-rank harness runs on one B200
+    local = int(os.environ.get("L4_FORCE_DEVICE", local))
+    backend = os.environ.get("L4_PIPE_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     if (ws > 1 and not args.replicas) or args.pipeline:
         if ws == 1:
             import socket

@@ -559,15 +559,18 @@ class DeviceOps:
         if not sends and not recvs:
             return 0
         pb = pool["view"].page_bytes
+        # NCCL moves device buffers over NVLink; the gloo backend (development: several ranks
+        # sharing one GPU) needs host buffers, so the staging goes through host memory there.
+        host = dist.get_backend() == "gloo"
         ops, bufs, nbytes = [], [], 0
         for dst, pages in sends:
             st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device=self.device)
             if pages:
                 l4.pack_pages(pool["view"], pages, st)
-            ops.append(dist.P2POp(dist.isend, st, dst))
+            ops.append(dist.P2POp(dist.isend, st.cpu() if host else st, dst))
             nbytes += len(pages) * 2 * pb
         for src, pages in recvs:
-            st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device=self.device)
+            st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device="cpu" if host else self.device)
             ops.append(dist.P2POp(dist.irecv, st, src))
             bufs.append((pages, st))
             nbytes += len(pages) * 2 * pb
@@ -575,5 +578,5 @@ class DeviceOps:
             w.wait()
         for pages, st in bufs:
             if pages:
-                l4.unpack_pages(pool["view"], pages, st)
+                l4.unpack_pages(pool["view"], pages, st.to(self.device) if host else st)
         return nbytes
