@@ -59,7 +59,10 @@ constexpr int kQSlotBytes = kMaxG * kHeadDim * 2;     // 2 KB
 constexpr int kMergeStride = kHeadDim + 4;            // floats per head row (bank-conflict padding)
 constexpr int kMaxSplits = 512;                       // per (request, kv head); lse staging capacity
 constexpr int kMinChunk = 8;                          // pages
-constexpr int kItemsPerCta = 8;                       // automatic chunk target
+#ifndef L4_ITEMS_PER_CTA
+#define L4_ITEMS_PER_CTA 8
+#endif
+constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
 // Guided tail (planner): split the last requests of the LPT order into chunks of ~per-CTA/16.
 // Measured r1: with the synchronous split epilogue it costs more than it saves (C2 151 -> 164 us),
@@ -380,7 +383,9 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
   const int Ct = (int)max((long long)kMinTailChunk, min((long long)C, (per_cta + kTailDiv - 1) / kTailDiv));
   const long long tail_budget = auto_mode ? (long long)kTailChunksPerCta * a.num_ctas * Ct : 0;
   int tail_requests = 0;
-  {
+  if (kTailChunksPerCta == 0) {  // guided tail compiled out: plain splits
+    for (int r = tid; r < a.B; r += nthr) s_ns[r] = nsplit_of(pages_of(s_len[s_rb[r]]), C);
+  } else {
     long long carry = 0, extra = 0;
     int ntail = 0;
     for (int tile = 0; tile < a.B; tile += nthr) {  // exclusive prefix of page-heads in rank order
