@@ -88,13 +88,31 @@ typedef struct {
   int32_t chunk_pages;    /* 0 = automatic length-binned split; > 0 forces the split
                              chunk C (pages per work item); < 0 = never split.  Requests
                              of <= 2C pages are never split (no combine needed). */
+  int32_t flags;          /* 0 or L4_DECODE_EARLY_INPUTS */
 } l4_decode_params;
+
+/* l4_decode_attention (single-launch path) may start reading its INPUTS (q, the KV pools,
+ * kv_len, page_indptr, page_indices) while the previous kernel on the stream is still
+ * running (programmatic dependent launch), so in a loop of calls the next call's planning
+ * and first page loads overlap the previous call's tail.  Outputs and the workspace are
+ * still touched only after the previous kernel has completed.  Set it only when the kernel
+ * launched immediately before on the same stream cannot be writing those inputs (another
+ * l4 call, or any kernel that does not itself trigger programmatic launch early). */
+enum { L4_DECODE_EARLY_INPUTS = 1 };
 
 /* Bytes of device workspace needed for any batch whose page table has at most
  * max_total_pages entries (indptr[B] <= max_total_pages).  Returns 0 if the
  * params are invalid (see l4_last_error()).  Must be queried with the target
- * device current (the bound depends on its SM count). */
+ * device current (the bound depends on its SM count).
+ * A workspace is caller-owned device memory.  It must be zero-filled once before its
+ * first use (l4_decode_workspace_init, or any zero fill); every completed call leaves
+ * its scheduler state and split counters zero again, so it can then be reused by any
+ * number of calls with the same num_kv_heads and any batch <= 8192. */
 size_t l4_decode_workspace_size(const l4_decode_params* p, int64_t max_total_pages);
+
+/* Zero the workspace's scheduler header and split counters (cudaMemsetAsync on `stream`). */
+l4_status l4_decode_workspace_init(const l4_decode_params* p, void* workspace, size_t workspace_bytes,
+                                   void* stream);
 
 /* a1: build the length-binned work list for this step from device kv_len [B]
  * and page_indptr [B+1] into `workspace` (one device kernel, graph-capturable,
@@ -112,7 +130,12 @@ l4_status l4_decode_run(const l4_decode_params* p, const void* q, const void* k_
                         int64_t num_pages, const int32_t* page_indices, void* out, float* lse,
                         void* workspace, size_t workspace_bytes, void* stream);
 
-/* Convenience: l4_decode_plan followed by l4_decode_run (one decode iteration). */
+/* One decode iteration in ONE kernel launch (a1 + a2 + a3): for B <= 1024 every CTA of the
+ * persistent split-KV kernel builds the same length-binned plan in its own shared memory
+ * from kv_len / page_indptr (no planner launch, no global work list, no host sync); larger
+ * batches run l4_decode_plan then l4_decode_run.  Identical results to plan + run (same
+ * work list, same reduction order).  Does not leave a reusable plan in the workspace:
+ * call l4_decode_plan before l4_decode_run. */
 l4_status l4_decode_attention(const l4_decode_params* p, const void* q, const void* k_pages,
                               const void* v_pages, int64_t num_pages, const int32_t* page_indptr,
                               const int32_t* page_indices, int64_t total_pages, const int32_t* kv_len,

@@ -64,12 +64,6 @@ constexpr int kMinChunk = 8;                          // pages
 #endif
 constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
-// Guided tail (planner): split the last requests of the LPT order into chunks of ~per-CTA/16.
-// Measured r1: with the synchronous split epilogue it costs more than it saves (C2 151 -> 164 us),
-// so it is disabled (kTailChunksPerCta = 0) until the epilogue is asynchronous.
-constexpr int kTailChunksPerCta = 0;
-constexpr int kTailDiv = 16;
-constexpr int kMinTailChunk = 4;                      // pages
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
 constexpr int kNumBins = 32;
@@ -80,6 +74,20 @@ struct __align__(16) WorkItem {
   int b, h, pbeg, pend, last_valid, part_base, nsplit, split;
 };
 static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
+
+#ifdef L4_TRACE
+// Development-only timeline probe (scripts/trace_fused.py): %globaltimer at fixed points of
+// every CTA, built only into trace variants (scripts/build_variant.sh ... -DL4_TRACE).
+__device__ unsigned long long g_trace[4096 * 16];
+__device__ __forceinline__ void trace_mark(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_trace[blockIdx.x * 16 + k] = t;
+}
+#define L4_MARK(k) trace_mark(k)
+#else
+#define L4_MARK(k) ((void)0)
+#endif
 
 // Header region (256 B): plan summary + dynamic scheduler state.
 struct __align__(16) PlanHeader {
@@ -103,7 +111,10 @@ WsLayout ws_layout(int B, int Hkv, int G, int items_cap) {
   L.items_cap = items_cap;
   L.header = 0;
   L.counters = 256;
-  L.items = align256(L.counters + (size_t)std::max(B, 1) * Hkv * sizeof(int));
+  // counters are self-cleaning across runs, so their region must not depend on B: a workspace
+  // reused with another batch size never sees stale items where its counters are
+  (void)B;
+  L.items = align256(L.counters + (size_t)kMaxBatch * Hkv * sizeof(int));
   L.part_lse = align256(L.items + (size_t)items_cap * sizeof(WorkItem));
   L.part_o = align256(L.part_lse + (size_t)items_cap * G * sizeof(float));
   L.total = align256(L.part_o + (size_t)items_cap * G * kHeadDim * sizeof(float));
@@ -149,6 +160,7 @@ l4_status check_params(const l4_decode_params* p, int* G_out) {
   if (!(G == 1 || G == 2 || G == 4 || G == 8)) return fail(L4_ERR_UNSUPPORTED, "GQA group must be 1, 2, 4 or 8");
   L4_CHECK_ARG(p->out_dtype == L4_DT_F32 || p->out_dtype == L4_DT_BF16, "out_dtype must be F32 or BF16");
   L4_CHECK_ARG(std::isfinite(p->sm_scale), "sm_scale must be finite");
+  L4_CHECK_ARG((p->flags & ~L4_DECODE_EARLY_INPUTS) == 0, "unknown decode flags");
   *G_out = G;
   return L4_OK;
 }
@@ -166,8 +178,7 @@ int items_cap_for(const l4_decode_params* p, int64_t max_total_pages, int num_ct
   } else {
     // C >= T*Hkv/(W*k) => Hkv * sum ceil(p_b / C) <= W*k + Hkv*B
     cap = std::min(Hkv * (B + ceil_div64(max_total_pages, kMinChunk)),
-                   Hkv * B + (int64_t)num_ctas * kItemsPerCta + Hkv) +
-          (int64_t)num_ctas * kTailChunksPerCta + (kTailChunksPerCta > 0 ? Hkv * B : 0);  // guided-tail splits
+                   Hkv * B + (int64_t)num_ctas * kItemsPerCta + Hkv);
   }
   cap = std::max<int64_t>(cap, 1);
   return (int)std::min<int64_t>(cap, INT_MAX / 64);
@@ -184,35 +195,6 @@ struct PlanArgs {
 };
 
 constexpr int kPlanMaxWarps = kPlanThreads / 32;
-
-// Block-wide exclusive scan of one int per thread; returns the prefix, writes the total.
-__device__ int block_excl_scan(int v, int* total, int* s_warp) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  __syncthreads();
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    const int w = lane < nw ? s_warp[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += t;
-    }
-    if (lane < nw) s_warp[lane] = wi - w;
-    if (lane == 31) s_warp[32] = wi;
-  }
-  __syncthreads();
-  *total = s_warp[32];
-  return s_warp[warp] + incl - v;
-}
 
 // Block-wide (sum int64, max int, or bits) in one pass.
 __device__ void block_reduce3(long long v, int m, unsigned bits, long long* s_ll, int* s_i, unsigned* s_u,
@@ -258,196 +240,221 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
   return min(kNumBins - 1, 32 - __clz(ip));      // bit_length(ip)
 }
 
-// One CTA of 1024 threads.  Requests are ordered by length bin, longest bin
-// first, and by request index inside a bin (deterministic plans); each request
-// contributes nsplit * Hkv items, contiguous per (request, kv head).
-__global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
-  // PDL: let the dependent decode kernel start its prologue now; it waits
-  // (griddepcontrol.wait) for this grid's completion before reading the plan.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  extern __shared__ int plan_smem[];  // s_len, s_ptr, s_rb (request at rank), s_off, s_ns (splits at rank)
-  const int Bs = max(a.B, 1);
-  int* s_len = plan_smem;
-  int* s_ptr = plan_smem + Bs;
-  int* s_rb = plan_smem + 2 * Bs;
-  int* s_off = plan_smem + 3 * Bs;
-  int* s_ns = plan_smem + 4 * Bs;
-  __shared__ long long s_ll[32];
-  __shared__ int s_i[33];
-  __shared__ unsigned s_u[32];
-  __shared__ int s_hist[kNumBins];
-  __shared__ int s_binbase[kNumBins];
-  __shared__ int s_wb[kPlanMaxWarps][kNumBins];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nthr = blockDim.x, nwarps = nthr >> 5;
-  for (int b = tid; b < a.B; b += nthr) {
-    s_len[b] = a.kv_len[b];
-    s_ptr[b] = a.indptr[b];
-  }
-  if (tid < kNumBins) s_hist[tid] = 0;
-  __syncthreads();
+// Shared-memory scratch of plan_core (bytes; 8-byte aligned base).
+constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4;
 
+// The planner (a1), run by every thread of a CTA: reads kv_len / indptr, chooses the chunk C,
+// and orders the requests by length bin, longest bin first, request index ascending inside a
+// bin (deterministic).  Leaves in shared memory: s_len / s_ptr [B] (kv_len, indptr), s_rb [B]
+// (request at rank r | its split count << 16), s_off [B+1] (first item of rank r; rank r owns nsplit * Hkv items,
+// contiguous per kv head), and returns C, the item count N and the largest page count.
+// Used by plan_kernel (materialised work list) and by the fused decode kernel (every CTA
+// plans redundantly in its own shared memory: no planner launch, no global work list).
+// Ranking is warp-blocked (warp w owns a contiguous range of requests): ~10 block barriers
+// whatever B is.
+__device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict__ indptr, int B, int Hkv,
+                          int num_ctas, int forced_chunk, int items_cap, int* s_len, int* s_ptr, int* s_rb,
+                          int* s_off, unsigned char* scratch, int* C_out, int* N_out, int* Pmax_out) {
+  long long* s_ll = reinterpret_cast<long long*>(scratch);
+  int* s_i = reinterpret_cast<int*>(scratch + 32 * 8);
+  unsigned* s_u = reinterpret_cast<unsigned*>(scratch + 32 * 8 + 36 * 4);
+  int* s_wcnt = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4);  // [nw][kNumBins]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x, nw = nthr >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
   long long T;
   int Pmax;
   unsigned unused;
   {
     long long sum = 0;
     int mx = 0;
-    for (int b = tid; b < a.B; b += nthr) {
-      const int pg = pages_of(s_len[b]);
+    for (int b = tid; b < B; b += nthr) {
+      const int L = kv_len[b];
+      s_len[b] = L;
+      s_ptr[b] = indptr[b];
+      const int pg = pages_of(L);
       sum += pg;
       mx = max(mx, pg);
     }
-    block_reduce3(sum, mx, 0u, s_ll, s_i, s_u, &T, &Pmax, &unused);
+    for (int x = tid; x < nw * kNumBins; x += nthr) s_wcnt[x] = 0;
+    block_reduce3(sum, mx, 0u, s_ll, s_i, s_u, &T, &Pmax, &unused);  // its barriers publish s_len/s_ptr
   }
+  if (tid == 0) L4_MARK(6);
   // chunk size C (pages per work item)
   long long Cl;
-  if (a.forced_chunk > 0) {
-    Cl = a.forced_chunk;
-  } else if (a.forced_chunk < 0) {
+  if (forced_chunk > 0) {
+    Cl = forced_chunk;
+  } else if (forced_chunk < 0) {
     Cl = INT_MAX / 4;
   } else {
-    const long long denom = (long long)a.num_ctas * kItemsPerCta;
-    Cl = max((long long)kMinChunk, (T * a.Hkv + denom - 1) / denom);
+    const long long denom = (long long)num_ctas * kItemsPerCta;
+    Cl = max((long long)kMinChunk, (T * Hkv + denom - 1) / denom);
   }
   Cl = max(Cl, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
   int C = (int)min(Cl, (long long)(INT_MAX / 4));
+  // ---- ranks: counting sort by bin (descending), stable in request order.  Warp w owns the
+  // contiguous request range [r0, r1); pass 1 also counts the items, so growing C when the
+  // work list does not fit the workspace repeats pass 1 only (block-uniform loop).
+  const int tiles = (B + 31) >> 5;
+  const int tpw = (tiles + nw - 1) / nw;
+  const int r0 = min(B, warp * tpw * 32), r1 = min(B, r0 + tpw * 32);
   long long N;
-  for (;;) {  // grow C until the work list fits the workspace (block-uniform loop)
-    long long items = 0;
-    for (int b = tid; b < a.B; b += nthr) items += (long long)nsplit_of(pages_of(s_len[b]), C) * a.Hkv;
-    int dummy;
-    block_reduce3(items, 0, 0u, s_ll, s_i, s_u, &N, &dummy, &unused);
-    if (N <= a.items_cap || C >= INT_MAX / 8) break;
-    C *= 2;
-  }
-
-  // ---- ranks: requests per bin, bins in descending order
-  for (int t0 = 0; t0 < a.B; t0 += nthr) {  // warp-aggregated histogram of bins
-    const int b = t0 + tid;
-    int bin = -1;
-    if (b < a.B) {
-      const int pg = pages_of(s_len[b]);
-      bin = bin_of(pg, nsplit_of(pg, C));
+  for (;;) {
+    int wsum = 0;
+    for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 1: per-warp bin histogram + item count
+      const int b = t0 + lane;
+      int bin = -1;
+      if (b < r1) {
+        const int pg = pages_of(s_len[b]);
+        const int ns = nsplit_of(pg, C);
+        bin = bin_of(pg, ns);
+        wsum += ns;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (bin >= 0 && (peers & lt_mask) == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
+      __syncwarp();
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    if (bin >= 0 && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[bin], __popc(peers));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if (lane == 0) s_i[warp] = wsum;
+    __syncthreads();
+    N = 0;
+    for (int w = 0; w < nw; ++w) N += s_i[w];
+    N *= Hkv;
+    if (N <= items_cap || C >= INT_MAX / 8) break;
+    C *= 2;
+    for (int x = tid; x < nw * kNumBins; x += nthr) s_wcnt[x] = 0;
+    __syncthreads();
   }
-  __syncthreads();
-  if (warp == 0) {  // exclusive scan over bins, highest bin first
+  if (tid == 0) L4_MARK(7);
+  if (warp == 0) {  // bases: bins in descending order, then warps in request order
     const int bin = kNumBins - 1 - lane;
-    const int h = s_hist[bin];
-    int incl = h;
+    int tot = 0;
+    for (int w = 0; w < nw; ++w) tot += s_wcnt[w * kNumBins + bin];
+    int incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    s_binbase[bin] = incl - h;
+    int base = incl - tot;
+    for (int w = 0; w < nw; ++w) {
+      const int c = s_wcnt[w * kNumBins + bin];
+      s_wcnt[w * kNumBins + bin] = base;
+      base += c;
+    }
   }
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int tile = 0; tile < a.B; tile += nthr) {  // block-uniform
-    const int b = tile + tid;
-    int bin = -1;
-    if (b < a.B) {
+  __syncthreads();
+  if (tid == 0) L4_MARK(8);
+  for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
+    const int b = t0 + lane;
+    int bin = -1, ns = 0;
+    if (b < r1) {
       const int pg = pages_of(s_len[b]);
-      bin = bin_of(pg, nsplit_of(pg, C));
+      ns = nsplit_of(pg, C);
+      bin = bin_of(pg, ns);
     }
     const unsigned peers = __match_any_sync(0xffffffffu, bin);
     const int lower = __popc(peers & lt_mask);
-    __syncthreads();  // previous tile finished with s_wb / s_binbase
-    for (int x = tid; x < nwarps * kNumBins; x += nthr) (&s_wb[0][0])[x] = 0;
-    __syncthreads();
-    if (bin >= 0 && lower == 0) s_wb[warp][bin] = __popc(peers);
-    __syncthreads();
-    if (tid < kNumBins) {  // per bin: exclusive running count over warps (request order)
-      int run = 0;
-      for (int w = 0; w < nwarps; ++w) {
-        const int c = s_wb[w][tid];
-        s_wb[w][tid] = run;
-        run += c;
-      }
-      s_i[tid] = run;  // this tile's requests in bin tid
+    int pos = 0;
+    if (bin >= 0) pos = s_wcnt[warp * kNumBins + bin] + lower;
+    __syncwarp();
+    if (bin >= 0) {
+      s_rb[pos] = b | (ns << 16);  // b < 8192, ns <= kMaxSplits
+      if (lower == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
     }
-    __syncthreads();
-    if (bin >= 0) s_rb[s_binbase[bin] + s_wb[warp][bin] + lower] = b;
-    __syncthreads();
-    if (tid < kNumBins) s_binbase[tid] += s_i[tid];
+    __syncwarp();
   }
   __syncthreads();
-  // ---- guided tail: the requests processed last (the suffix of the LPT order holding about
-  // kTailChunksPerCta chunks of C_tail pages per CTA) are split into C_tail-page chunks so that
-  // all CTAs finish within a small item of each other (auto mode only).
-  const bool auto_mode = a.forced_chunk == 0;
-  const long long per_cta = (T * a.Hkv + a.num_ctas - 1) / max(a.num_ctas, 1);
-  const int Ct = (int)max((long long)kMinTailChunk, min((long long)C, (per_cta + kTailDiv - 1) / kTailDiv));
-  const long long tail_budget = auto_mode ? (long long)kTailChunksPerCta * a.num_ctas * Ct : 0;
-  int tail_requests = 0;
-  if (kTailChunksPerCta == 0) {  // guided tail compiled out: plain splits
-    for (int r = tid; r < a.B; r += nthr) s_ns[r] = nsplit_of(pages_of(s_len[s_rb[r]]), C);
-  } else {
-    long long carry = 0, extra = 0;
-    int ntail = 0;
-    for (int tile = 0; tile < a.B; tile += nthr) {  // exclusive prefix of page-heads in rank order
-      const int r = tile + tid;
-      const int pg = r < a.B ? pages_of(s_len[s_rb[r]]) : 0;
-      int tot;
-      const int ex = block_excl_scan(pg, &tot, s_i);
-      if (r < a.B) {
-        const long long suffix = (T - (carry + ex)) * a.Hkv;  // page-heads from rank r to the end
-        int ns = nsplit_of(pg, C);
-        if (suffix <= tail_budget && pg > 0) {
-          const int nt = min(nsplit_of(pg, Ct), kMaxSplits);
-          if (nt > ns) {
-            extra += (long long)(nt - ns) * a.Hkv;
-            ns = nt;
-          }
-          ntail += 1;
-        }
-        s_ns[r] = ns;
-      }
-      carry += tot;
-    }
-    long long ex_tot;
-    int ntail_tot;
-    unsigned unused2;
-    block_reduce3(extra, ntail, 0u, s_ll, s_i, s_u, &ex_tot, &ntail_tot, &unused2);
-    // block_reduce3's max is not a sum: count tail requests with a second pass
-    int cnt = 0;
-    for (int r = tid; r < a.B; r += nthr) cnt += s_ns[r] != nsplit_of(pages_of(s_len[s_rb[r]]), C) ? 1 : 0;
-    long long cnt_ll;
-    int dummy2;
-    block_reduce3(cnt, 0, 0u, s_ll, s_i, s_u, &cnt_ll, &dummy2, &unused2);
-    if (N + ex_tot > a.items_cap) {  // no room: keep the plain plan
-      for (int r = tid; r < a.B; r += nthr) s_ns[r] = nsplit_of(pages_of(s_len[s_rb[r]]), C);
-      ex_tot = 0;
-      cnt_ll = 0;
-    }
-    N += ex_tot;
-    tail_requests = (int)cnt_ll;
-  }
-  __syncthreads();
-  // ---- item offsets: exclusive scan of nsplit * Hkv in rank order
+  if (tid == 0) L4_MARK(9);
+  // ---- item offsets: exclusive scan of nsplit * Hkv in rank order (same warp ranges)
   {
-    int carry = 0;
-    for (int tile = 0; tile < a.B; tile += nthr) {
-      const int r = tile + tid;
-      int cnt = 0;
-      if (r < a.B) cnt = s_ns[r] * a.Hkv;
-      int tot;
-      const int ex = block_excl_scan(cnt, &tot, s_i);
-      if (r < a.B) s_off[r] = carry + ex;
-      carry += tot;
+    int wsum = 0;
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+      const int r = t0 + lane;
+      wsum += r < r1 ? (s_rb[r] >> 16) : 0;
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if (lane == 0) s_i[warp] = wsum;  // pass 1's counts in s_i were read two barriers ago
+    __syncthreads();
+    int carry = 0;
+    for (int w = 0; w < warp; ++w) carry += s_i[w];
+    carry *= Hkv;
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+      const int r = t0 + lane;
+      const int cnt = r < r1 ? (s_rb[r] >> 16) * Hkv : 0;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (r < r1) s_off[r] = carry + incl - cnt;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) s_off[B] = (int)N;
   }
   __syncthreads();
+  *C_out = C;
+  *N_out = (int)N;
+  *Pmax_out = Pmax;
+}
+
+// Work item `i` of the plan held in shared memory (fused path) — the same item plan_kernel
+// writes at index i: rank r = the last rank whose first item is <= i, then (kv head, split).
+__device__ __forceinline__ WorkItem item_from_plan(int i, int n, const int* s_len, const int* s_ptr,
+                                                   const int* s_rb, const int* s_off, int B, int C) {
+  WorkItem it;
+  if (i >= n) {
+    it.b = -1; it.h = 0; it.pbeg = 0; it.pend = 0; it.last_valid = 0; it.part_base = 0; it.nsplit = 1; it.split = 0;
+    return it;
+  }
+  int lo = 0, hi = B - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  const int b = s_rb[lo] & 0xffff, ns = s_rb[lo] >> 16;
+  const int L = s_len[b];
+  const int pg = pages_of(L);
+  const int loc = i - s_off[lo];
+  const int h = loc / ns, sp = loc - h * ns;
+  const int p0 = (sp * pg) / ns, p1 = ((sp + 1) * pg) / ns;
+  it.b = b;
+  it.h = h;
+  it.pbeg = s_ptr[b] + p0;
+  it.pend = s_ptr[b] + p1;
+  it.last_valid = p1 == pg ? (pg > 0 ? L - (pg - 1) * kPage : 0) : kPage;
+  it.part_base = s_off[lo] + h * ns;
+  it.nsplit = ns;
+  it.split = sp;
+  return it;
+}
+
+// Materialised plan: one CTA (<= 1024 threads) runs plan_core and writes the work list,
+// so one plan serves many l4_decode_run calls (e.g. every layer of a decode iteration).
+__global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
+  // PDL: let the dependent decode kernel start its prologue now; it waits
+  // (griddepcontrol.wait) for this grid's completion before reading the plan.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ __align__(16) unsigned char plan_smem_raw[];
+  const int Bs = max(a.B, 1);
+  unsigned char* scratch = plan_smem_raw;
+  int* s_len = reinterpret_cast<int*>(plan_smem_raw + kPlanScratchBytes);
+  int* s_ptr = s_len + Bs;
+  int* s_rb = s_ptr + Bs;
+  int* s_off = s_rb + Bs;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  int C, N, Pmax;
+  plan_core(a.kv_len, a.indptr, a.B, a.Hkv, a.num_ctas, a.forced_chunk, a.items_cap, s_len, s_ptr, s_rb, s_off,
+            scratch, &C, &N, &Pmax);
   // ---- items: one thread per (request rank, kv head) writes that pair's splits
   for (int x = tid; x < a.B * a.Hkv; x += nthr) {
     const int r = x / a.Hkv, h = x - r * a.Hkv;
-    const int b = s_rb[r];
+    const int b = s_rb[r] & 0xffff, ns = s_rb[r] >> 16;
     const int L = s_len[b];
     const int pg = pages_of(L);
-    const int ns = s_ns[r];
     const int first = s_off[r] + h * ns;
     const int pbase = s_ptr[b];
     const int last_valid = pg > 0 ? L - (pg - 1) * kPage : 0;
@@ -464,12 +471,10 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
   if (tid == 0) {
     PlanHeader hd;
     memset(&hd, 0, sizeof(hd));
-    hd.n_items = (int)N;
+    hd.n_items = N;
     hd.chunk = C;
     hd.num_ctas = a.num_ctas;
     hd.max_splits = nsplit_of(Pmax, C);
-    hd.tail_requests = tail_requests;
-    hd.tail_chunk = tail_requests > 0 ? Ct : 0;
     hd.batch = a.B;
     hd.num_kv_heads = a.Hkv;
     hd.items_cap = a.items_cap;
@@ -493,6 +498,11 @@ struct RunArgs {
   int Hq, Hkv;
   float scale_log2;  // sm_scale * log2(e)
   int out_bf16;
+  // fused path only: the planner's inputs (every CTA plans in shared memory)
+  const int* kv_len;
+  const int* indptr;
+  int B, forced_chunk, items_cap;
+  int early;  // L4_DECODE_EARLY_INPUTS: read inputs before griddepcontrol.wait (fused path)
 };
 
 struct __align__(16) SlotItem {  // item handed from the producer to the consumers
@@ -514,6 +524,11 @@ struct SmemLayout {
   static constexpr int alloc = total + 1024;  // room to align the base to 1024 B (128B swizzle)
 };
 static_assert(kMaxSplits * kMaxG * 4 <= kConsumerWarps * kMaxG * kMergeStride * 4, "lse staging fits merge area");
+static_assert(kPlanScratchBytes <= kConsumerWarps * kMaxG * kMergeStride * 4, "plan scratch fits merge area");
+static_assert(SmemLayout::merge_o % 8 == 0 && SmemLayout::total % 16 == 0, "plan areas aligned");
+// Fused path: plan arrays s_len, s_ptr, s_rb [B] and s_off [B+1] after the kernel's own layout.
+inline size_t fused_plan_bytes(int B) { return ((size_t)(4 * B + 1) * 4 + 15) & ~size_t(15); }
+constexpr int kFusedMaxBatch = 1024;  // 2 CTAs per SM still fit (2 x ~108 KB)
 
 __device__ __forceinline__ void store_out(const RunArgs& a, size_t idx, float v) {
   if (a.out_bf16)
@@ -622,7 +637,8 @@ __device__ __forceinline__ WorkItem load_item(const WorkItem* items, int i, int 
   return it;
 }
 
-template <int G>
+
+template <int G, bool kFused>
 __global__ void __launch_bounds__(kThreads, 2)
     decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, RunArgs a) {
   using namespace dev;
@@ -641,6 +657,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   volatile int* s_flag = reinterpret_cast<volatile int*>(smem + SmemLayout::flag);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) L4_MARK(0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(bar_full + i * 8, 1);
@@ -657,82 +674,157 @@ __global__ void __launch_bounds__(kThreads, 2)
     prefetch_tmap(&tmV);
   }
   __syncthreads();
-  // PDL: everything above overlapped the planner; the plan is read below.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // PDL: the next kernel in the stream may start its prologue as CTAs of this one retire; it
+  // waits (griddepcontrol.wait) for this grid to complete before touching memory.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // PDL: everything above overlapped the previous kernel (the planner, or the previous step).
+  // Early mode (fused only): the plan and the first item's loads read only the caller's inputs,
+  // which the previous kernel must not be writing (L4_DECODE_EARLY_INPUTS); every access to the
+  // workspace and every output write still comes after griddepcontrol.wait.
+  const bool early = kFused && a.early;
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) L4_MARK(1);
 
-  const int n_items = a.header->n_items;
   const int W = gridDim.x;
+  // producer lane 0: the first three scheduler tickets, in flight while the plan is built
+  int raw_t0 = -1, raw_t1 = -1, raw_t2 = -1;
+  if (!early && warp == kConsumerWarps && lane == 0) {
+    raw_t0 = atomicAdd(&a.header->sched_next, 1);
+    raw_t1 = atomicAdd(&a.header->sched_next, 1);
+    raw_t2 = atomicAdd(&a.header->sched_next, 1);
+  }
+  int n_items, plan_C = 0;
+  int *p_len = nullptr, *p_ptr = nullptr, *p_rb = nullptr, *p_off = nullptr;
+  if constexpr (kFused) {
+    // a1 in every CTA: the plan lives in this CTA's shared memory (scratch in the merge area,
+    // free until the first item finishes); no planner launch and no global work list.
+    p_len = reinterpret_cast<int*>(smem + SmemLayout::total);
+    p_ptr = p_len + a.B;
+    p_rb = p_ptr + a.B;
+    p_off = p_rb + a.B;
+    int pmax;
+    plan_core(a.kv_len, a.indptr, a.B, a.Hkv, W, a.forced_chunk, a.items_cap, p_len, p_ptr, p_rb, p_off,
+              smem + SmemLayout::merge_o, &plan_C, &n_items, &pmax);
+  } else {
+    n_items = a.header->n_items;
+  }
+  if (threadIdx.x == 0) L4_MARK(2);
+  auto get_item = [&](int i) -> WorkItem {
+    if constexpr (kFused)
+      return item_from_plan(i, n_items, p_len, p_ptr, p_rb, p_off, a.B, plan_C);
+    else
+      return load_item(a.items, i, n_items);
+  };
 
   if (warp == kConsumerWarps) {
     // ============================== producer warp: items, Q and KV pages via TMA
     const uint64_t policy = policy_evict_first();
     bool exhausted = false;
-    // Dynamic LPT scheduling: the first item is blockIdx.x, later ones come from
-    // an atomic ticket (W + ticket) so idle CTAs take the next-largest item.
-    auto draw = [&]() -> int {
-      int idx = n_items;
-      if (!exhausted) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(&a.header->sched_next, 1);
-        idx = W + __shfl_sync(0xffffffffu, t, 0);
-        if (idx >= n_items) {
-          exhausted = true;
-          idx = n_items;
-          if (lane == 0) {
-            const int done = atomicAdd(&a.header->sched_done, 1);
-            if (done == W - 1) {  // every CTA stopped drawing: reset for the next run
-              a.header->sched_next = 0;
-              a.header->sched_done = 0;
-            }
-          }
-        }
+    // Dynamic LPT scheduling: the first item is blockIdx.x, later ones come from an atomic
+    // ticket (W + ticket) so idle CTAs take the next-largest item.  Tickets are issued one
+    // item ahead of their use (three were issued before the plan was built), so no atomic
+    // round trip sits between two items or in front of the first TMA.  Every issued ticket
+    // is resolved (its value consumed) before this CTA reports done: the last CTA to report
+    // resets the scheduler for the next run.
+    auto resolve = [&](int raw) -> int {
+      const int t = __shfl_sync(0xffffffffu, raw, 0);
+      if (t < 0 || exhausted) return n_items;
+      if (W + t >= n_items) {
+        exhausted = true;
+        return n_items;
       }
-      return idx;
+      return W + t;
     };
+    auto issue = [&]() -> int {
+      int t = -1;
+      if (lane == 0 && !exhausted) t = atomicAdd(&a.header->sched_next, 1);
+      return t;
+    };
+    auto post_item = [&](uint32_t kk, const WorkItem& it, int idx) {  // lane 0: item + its Q rows
+      const uint32_t slot = kk % kItemSlots;
+      mbar_wait(bar_iempty + slot * 8, ((kk / kItemSlots) & 1) ^ 1);
+      SlotItem si;
+      si.it = it;
+      si.idx = idx;
+      s_items[slot] = si;
+      const uint32_t qbytes = G * kHeadDim * 2;
+      mbar_arrive_expect_tx(bar_ifull + slot * 8, qbytes);
+      bulk_load(sbase + SmemLayout::qslots + slot * kQSlotBytes,
+                a.q + ((size_t)it.b * a.Hq + (size_t)it.h * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
+    };
+    uint32_t qseq = 0;
+    auto issue_page = [&](int page, int h) {  // lane 0: one (page, kv head) K + V slice
+      const uint32_t st = qseq % kStages;
+      mbar_wait(bar_empty + st * 8, ((qseq / kStages) & 1) ^ 1);
+      const uint32_t fb = bar_full + st * 8;
+      mbar_arrive_expect_tx(fb, kStageBytes);
+      const int row = (page * a.Hkv + h) * kPage;
+      const uint32_t dst = sbase + SmemLayout::stages + st * kStageBytes;
+      tma_load_3d(dst, &tmK, 0, row, 0, fb, policy);
+      tma_load_3d(dst + kSliceBytes, &tmV, 0, row, 0, fb, policy);
+#ifdef L4_TRACE
+      if (qseq == 0) L4_MARK(3);
+#endif
+    };
+    // The first item (blockIdx.x: no ticket needed) goes out before anything else: its Q and
+    // its first kStages pages (early mode: all its pages, which may run while the previous
+    // kernel finishes) are in flight while the scheduler tickets resolve.
     int i_cur = blockIdx.x < n_items ? (int)blockIdx.x : n_items;
-    int i_nxt = draw();
-    WorkItem cur = load_item(a.items, i_cur, n_items);
-    WorkItem nxt = load_item(a.items, i_nxt, n_items);
-    int i_nn = draw();
+    if (i_cur >= n_items) exhausted = true;
+    WorkItem cur = get_item(i_cur);
     int cur_idx = (i_cur < n_items && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
-    uint32_t k = 0, qseq = 0;
-    for (; i_cur < n_items; ++k) {
-      // prefetch: the next item's first page ids, the item after's struct, one more ticket
-      const int nxt_idx = (i_nxt < n_items && lane < nxt.pend - nxt.pbeg) ? __ldg(a.indices + nxt.pbeg + lane) : 0;
-      const WorkItem nn = load_item(a.items, i_nn, n_items);
-      const int i_nnn = draw();
-      const uint32_t slot = k % kItemSlots;
-      if (lane == 0) {
-        mbar_wait(bar_iempty + slot * 8, ((k / kItemSlots) & 1) ^ 1);
-        SlotItem si;
-        si.it = cur;
-        si.idx = i_cur;
-        s_items[slot] = si;
-        const uint32_t qbytes = G * kHeadDim * 2;
-        mbar_arrive_expect_tx(bar_ifull + slot * 8, qbytes);
-        bulk_load(sbase + SmemLayout::qslots + slot * kQSlotBytes,
-                  a.q + ((size_t)cur.b * a.Hq + (size_t)cur.h * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
-      }
-      const int np = cur.pend - cur.pbeg;
+    int pre = 0;
+    if (i_cur < n_items) {
+      if (lane == 0) post_item(0, cur, i_cur);
+      const int np0 = cur.pend - cur.pbeg;
+      pre = early ? np0 : min(np0, kStages);
       int blk = cur_idx;
-      for (int j0 = 0; j0 < np; j0 += 32) {
-        const int nb = (j0 + 32 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + 32 + lane) : 0;
-        const int cnt = min(32, np - j0);
+      for (int j0 = 0; j0 < pre; j0 += 32) {
+        const int nb = (j0 + 32 + lane < np0) ? __ldg(a.indices + cur.pbeg + j0 + 32 + lane) : 0;
+        const int cnt = min(32, pre - j0);
         for (int j = 0; j < cnt; ++j) {
           const int page = __shfl_sync(0xffffffffu, blk, j);
-          if (lane == 0) {
-            const uint32_t st = qseq % kStages;
-            mbar_wait(bar_empty + st * 8, ((qseq / kStages) & 1) ^ 1);
-            const uint32_t fb = bar_full + st * 8;
-            mbar_arrive_expect_tx(fb, kStageBytes);
-            const int row = (page * a.Hkv + cur.h) * kPage;
-            const uint32_t dst = sbase + SmemLayout::stages + st * kStageBytes;
-            tma_load_3d(dst, &tmK, 0, row, 0, fb, policy);
-            tma_load_3d(dst + kSliceBytes, &tmV, 0, row, 0, fb, policy);
-          }
+          if (lane == 0) issue_page(page, cur.h);
           ++qseq;
         }
         blk = nb;
+      }
+    }
+    if (early) {  // from here on the scheduler state of the workspace is touched
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (lane == 0) {
+        raw_t0 = atomicAdd(&a.header->sched_next, 1);
+        raw_t1 = atomicAdd(&a.header->sched_next, 1);
+        raw_t2 = atomicAdd(&a.header->sched_next, 1);
+      }
+    }
+    int i_nxt = resolve(raw_t0);
+    WorkItem nxt = get_item(i_nxt);
+    int i_nn = resolve(raw_t1);
+    int raw_p = raw_t2;  // resolved in iteration 0
+    uint32_t k = 0;
+    for (; i_cur < n_items; ++k) {
+      // prefetch: the next item's first page ids, the item after's struct, one more ticket
+      const int nxt_idx = (i_nxt < n_items && lane < nxt.pend - nxt.pbeg) ? __ldg(a.indices + nxt.pbeg + lane) : 0;
+      const WorkItem nn = get_item(i_nn);
+      const int i_nnn = resolve(raw_p);  // issued one iteration ago
+      raw_p = issue();
+      if (k > 0 && lane == 0) post_item(k, cur, i_cur);
+      const int np = cur.pend - cur.pbeg;
+      const int jstart = k == 0 ? pre : 0;  // item 0's first `pre` pages went out above
+      if (jstart < np) {
+        int j0 = jstart & ~31;
+        int blk = j0 == 0 ? cur_idx : ((j0 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + lane) : 0);
+        for (; j0 < np; j0 += 32) {
+          const int nb = (j0 + 32 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + 32 + lane) : 0;
+          const int cnt = min(32, np - j0);
+          for (int j = max(jstart - j0, 0); j < cnt; ++j) {
+            const int page = __shfl_sync(0xffffffffu, blk, j);
+            if (lane == 0) issue_page(page, cur.h);
+            ++qseq;
+          }
+          blk = nb;
+        }
       }
       i_cur = i_nxt;
       cur = nxt;
@@ -741,7 +833,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       nxt = nn;
       i_nn = i_nnn;
     }
-    while (!exhausted) draw();  // make sure this CTA is counted as done
+    // the last issued ticket must complete before this CTA reports done
+    if (resolve(raw_p) != -7 && lane == 0) {
+      const int done = atomicAdd(&a.header->sched_done, 1);
+      if (done == W - 1) {  // every CTA stopped drawing: reset for the next run
+        a.header->sched_next = 0;
+        a.header->sched_done = 0;
+      }
+    }
     // sentinel: tell the consumers there is no more work
     if (lane == 0) {
       const uint32_t slot = k % kItemSlots;
@@ -788,12 +887,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t q = qbase + j;
       const uint32_t st = q % kStages;
       mbar_wait(bar_full + st * 8, (q / kStages) & 1);
+#ifdef L4_TRACE
+      if (q == 0 && lane == 0) L4_MARK(4);
+#endif
       const int valid = (j == np - 1) ? it.last_valid : kPage;
       consume_page(sbase + SmemLayout::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + st * 8);
     }
     qbase += np;
+    if (early && k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
 
     // ---- intra-CTA merge of the 4 warps' (m, l, O)
 #pragma unroll
@@ -909,6 +1012,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     named_bar_sync(1, kConsumerThreads);  // merge area free for the next item
   }
+  if (threadIdx.x == 0) L4_MARK(5);
 }
 
 // =================================================================== host side
@@ -949,15 +1053,17 @@ l4_status make_tmap(CUtensorMap* tm, const void* base, int64_t rows) {
   return L4_OK;
 }
 
-template <int G>
+template <int G, bool kFused>
 l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunArgs& a, int grid, cudaStream_t st) {
   static bool attr_set[64] = {false};
+  const size_t smem_max = SmemLayout::alloc + (kFused ? fused_plan_bytes(kFusedMaxBatch) : 0);
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemLayout::alloc);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<G, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_max);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(decode_kernel<G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      e = cudaFuncSetAttribute(decode_kernel<G, kFused>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -969,14 +1075,14 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunA
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = SmemLayout::alloc;
+  cfg.dynamicSmemBytes = SmemLayout::alloc + (kFused ? fused_plan_bytes(a.B) : 0);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: overlap with the planner
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: overlap with the previous kernel
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<G>, tk, tv, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<G, kFused>, tk, tv, a);
   if (e != cudaSuccess) {
     set_error("decode_kernel launch failed: %s", cudaGetErrorString(e));
     cudaGetLastError();
@@ -1031,6 +1137,29 @@ extern "C" size_t l4_decode_workspace_size(const l4_decode_params* p, int64_t ma
   return ws_layout(p->batch, p->num_kv_heads, G, cap).total;
 }
 
+#ifdef L4_TRACE
+extern "C" int l4_trace_read(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
+
+extern "C" l4_status l4_decode_workspace_init(const l4_decode_params* p, void* workspace, size_t workspace_bytes,
+                                             void* stream) {
+  int G = 0;
+  l4_status s = check_params(p, &G);
+  if (s != L4_OK) return s;
+  if (!workspace) return fail(L4_ERR_WORKSPACE, "workspace is NULL");
+  const size_t head = ws_layout(p->batch, p->num_kv_heads, G, 0).items;  // header + split counters
+  if (workspace_bytes < head) return fail(L4_ERR_WORKSPACE, "workspace too small");
+  cudaError_t e = cudaMemsetAsync(workspace, 0, head, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error("cudaMemsetAsync: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return L4_ERR_CUDA;
+  }
+  return L4_OK;
+}
+
 static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, const int32_t* page_indptr,
                            int64_t total_pages, void* workspace, size_t workspace_bytes, cudaStream_t st) {
   int G = 0;
@@ -1060,10 +1189,11 @@ static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, con
   a.header = reinterpret_cast<PlanHeader*>(ws + L.header);
   a.items = reinterpret_cast<WorkItem*>(ws + L.items);
   a.counters = reinterpret_cast<int*>(ws + L.counters);
-  const size_t smem = (size_t)5 * std::max(p->batch, 1) * sizeof(int);
+  const size_t smem = kPlanScratchBytes + ((size_t)4 * std::max(p->batch, 1) + 1) * sizeof(int);
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * kMaxBatch * (int)sizeof(int));
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPlanScratchBytes + (4 * kMaxBatch + 1) * (int)sizeof(int));
     // same L1/shared carveout as decode_kernel: no SM reconfiguration between the two launches
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   });
@@ -1078,24 +1208,37 @@ static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, con
   return L4_OK;
 }
 
+// Shared by l4_decode_run (plan read from the workspace) and the fused l4_decode_attention
+// (kv_len / page_indptr != NULL: every CTA plans in shared memory).
 static l4_status run_impl(const l4_decode_params* p, const void* q, const void* k_pages, const void* v_pages,
                           int64_t num_pages, const int32_t* page_indices, void* out, float* lse, void* workspace,
-                          size_t workspace_bytes, cudaStream_t st) {
+                          size_t workspace_bytes, cudaStream_t st, const int32_t* kv_len = nullptr,
+                          const int32_t* page_indptr = nullptr, int64_t total_pages = 0) {
   int G = 0;
   l4_status s = check_params(p, &G);
   if (s != L4_OK) return s;
   if (p->batch == 0) return L4_OK;
+  const bool fused = kv_len != nullptr;
   // page_indices may be NULL only when every request is empty (indptr[B] == 0).
   L4_CHECK_ARG(q && k_pages && v_pages && out, "q/k_pages/v_pages/out is NULL");
   L4_CHECK_ARG(num_pages >= 1, "num_pages must be >= 1");
   L4_CHECK_ARG((reinterpret_cast<uintptr_t>(q) & 15) == 0, "q must be 16-byte aligned");
   if (!workspace) return fail(L4_ERR_WORKSPACE, "workspace is NULL");
-  WsLayout L;
-  if (!ws_layout_from_bytes(p->batch, p->num_kv_heads, G, workspace_bytes, &L))
-    return fail(L4_ERR_WORKSPACE, "workspace too small");
   int ctas = 0;
   s = device_ctas(&ctas);
   if (s != L4_OK) return s;
+  WsLayout L;
+  if (fused) {
+    L4_CHECK_ARG(page_indptr != nullptr, "page_indptr is NULL");
+    L4_CHECK_ARG(total_pages >= 0, "total_pages < 0");
+    const size_t need = ws_layout(p->batch, p->num_kv_heads, G, items_cap_for(p, total_pages, ctas)).total;
+    if (workspace_bytes < need || !ws_layout_from_bytes(p->batch, p->num_kv_heads, G, workspace_bytes, &L)) {
+      set_error("workspace too small: %zu < %zu bytes (l4_decode_workspace_size)", workspace_bytes, need);
+      return L4_ERR_WORKSPACE;
+    }
+  } else if (!ws_layout_from_bytes(p->batch, p->num_kv_heads, G, workspace_bytes, &L)) {
+    return fail(L4_ERR_WORKSPACE, "workspace too small");
+  }
   const int64_t rows = num_pages * p->num_kv_heads * kPage;
   CUtensorMap tk, tv;
   s = make_tmap(&tk, k_pages, rows);
@@ -1104,6 +1247,7 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   if (s != L4_OK) return s;
   char* ws = static_cast<char*>(workspace);
   RunArgs a;
+  memset(&a, 0, sizeof(a));
   a.q = static_cast<const __nv_bfloat16*>(q);
   a.out = out;
   a.lse = lse;
@@ -1118,11 +1262,25 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   const float scale = p->sm_scale > 0.f ? p->sm_scale : 1.0f / std::sqrt((float)kHeadDim);
   a.scale_log2 = scale * kLog2e;
   a.out_bf16 = p->out_dtype == L4_DT_BF16;
+  a.kv_len = kv_len;
+  a.indptr = page_indptr;
+  a.B = p->batch;
+  a.forced_chunk = p->chunk_pages;
+  a.items_cap = L.items_cap;
+  a.early = fused && (p->flags & L4_DECODE_EARLY_INPUTS) != 0;
+  if (fused) {
+    switch (G) {
+      case 1: return launch_decode<1, true>(tk, tv, a, ctas, st);
+      case 2: return launch_decode<2, true>(tk, tv, a, ctas, st);
+      case 4: return launch_decode<4, true>(tk, tv, a, ctas, st);
+      default: return launch_decode<8, true>(tk, tv, a, ctas, st);
+    }
+  }
   switch (G) {
-    case 1: return launch_decode<1>(tk, tv, a, ctas, st);
-    case 2: return launch_decode<2>(tk, tv, a, ctas, st);
-    case 4: return launch_decode<4>(tk, tv, a, ctas, st);
-    default: return launch_decode<8>(tk, tv, a, ctas, st);
+    case 1: return launch_decode<1, false>(tk, tv, a, ctas, st);
+    case 2: return launch_decode<2, false>(tk, tv, a, ctas, st);
+    case 4: return launch_decode<4, false>(tk, tv, a, ctas, st);
+    default: return launch_decode<8, false>(tk, tv, a, ctas, st);
   }
 }
 
@@ -1147,6 +1305,13 @@ extern "C" l4_status l4_decode_attention(const l4_decode_params* p, const void* 
                                          const int32_t* page_indices, int64_t total_pages, const int32_t* kv_len,
                                          void* out, float* lse, void* workspace, size_t workspace_bytes,
                                          void* stream) {
+  // One launch: every CTA of the decode kernel plans in its own shared memory (B <= 1024).
+  // Larger batches: the materialised plan (planner kernel) followed by the run.
+  if (p && p->batch > 0 && p->batch <= kFusedMaxBatch) {
+    L4_CHECK_ARG(kv_len != nullptr, "kv_len is NULL");
+    return run_impl(p, q, k_pages, v_pages, num_pages, page_indices, out, lse, workspace, workspace_bytes,
+                    static_cast<cudaStream_t>(stream), kv_len, page_indptr, total_pages);
+  }
   l4_status s = l4_decode_plan(p, kv_len, page_indptr, total_pages, workspace, workspace_bytes, stream);
   if (s != L4_OK) return s;
   return l4_decode_run(p, q, k_pages, v_pages, num_pages, page_indices, out, lse, workspace, workspace_bytes, stream);
@@ -1178,7 +1343,7 @@ extern "C" l4_status l4_decode_plan_items(const void* workspace, int32_t* items_
   cudaError_t e = cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess) {
-    const size_t items_off = align256(256 + (size_t)std::max(h.batch, 1) * h.num_kv_heads * sizeof(int));
+    const size_t items_off = align256(256 + (size_t)kMaxBatch * h.num_kv_heads * sizeof(int));
     const int n = std::min(h.n_items, max_items);
     if (n > 0)
       e = cudaMemcpyAsync(items_out, static_cast<const char*>(workspace) + items_off, (size_t)n * sizeof(WorkItem),

@@ -18,10 +18,11 @@ LIB_PATH = os.environ.get("L4_LIB") or os.path.join(_HERE, "libl4.so")  # L4_LIB
 
 L4_OK, L4_ERR_INVALID_ARG, L4_ERR_UNSUPPORTED, L4_ERR_CUDA, L4_ERR_WORKSPACE, L4_ERR_NO_PAGES, L4_ERR_INFEASIBLE = range(7)
 L4_DT_F32, L4_DT_BF16 = 0, 1
+L4_DECODE_EARLY_INPUTS = 1
 _STATUS_NAMES = ["OK", "INVALID_ARG", "UNSUPPORTED", "CUDA", "WORKSPACE", "NO_PAGES", "INFEASIBLE"]
 
 EXPORTED_SYMBOLS = (
-    "l4_last_error", "l4_version", "l4_decode_workspace_size", "l4_decode_plan", "l4_decode_run",
+    "l4_last_error", "l4_version", "l4_decode_workspace_size", "l4_decode_workspace_init", "l4_decode_plan", "l4_decode_run",
     "l4_decode_attention", "l4_decode_plan_info", "l4_decode_plan_items", "l4_partition", "l4_pool_create",
     "l4_pool_alloc", "l4_pool_free", "l4_pool_num_free", "l4_pool_destroy", "l4_migrate", "l4_copy_pages",
     "l4_pack_pages", "l4_unpack_pages", "l4_ipc_get_handle", "l4_ipc_open_handle", "l4_ipc_close_handle",
@@ -43,7 +44,7 @@ class NoPagesError(L4Error):
 class DecodeParams(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("page_size", ctypes.c_int32), ("sm_scale", ctypes.c_float),
-                ("out_dtype", ctypes.c_int32), ("chunk_pages", ctypes.c_int32)]
+                ("out_dtype", ctypes.c_int32), ("chunk_pages", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -92,6 +93,8 @@ def lib() -> ctypes.CDLL:
     L.l4_version.restype = ctypes.c_char_p
     L.l4_decode_workspace_size.restype = sz
     L.l4_decode_workspace_size.argtypes = [P(DecodeParams), i64]
+    L.l4_decode_workspace_init.restype = ctypes.c_int
+    L.l4_decode_workspace_init.argtypes = [P(DecodeParams), vp, sz, vp]
     L.l4_decode_plan.restype = ctypes.c_int
     L.l4_decode_plan.argtypes = [P(DecodeParams), vp, vp, i64, vp, sz, vp]
     L.l4_decode_run.restype = ctypes.c_int
@@ -177,8 +180,10 @@ def _need(t, dtype, name, device=True):
 
 
 def make_params(batch: int, num_q_heads: int, num_kv_heads: int, head_dim: int = 128, page_size: int = 16,
-                sm_scale: float = 0.0, out_dtype: int = L4_DT_F32, chunk_pages: int = 0) -> DecodeParams:
-    return DecodeParams(batch, num_q_heads, num_kv_heads, head_dim, page_size, sm_scale, out_dtype, chunk_pages)
+                sm_scale: float = 0.0, out_dtype: int = L4_DT_F32, chunk_pages: int = 0,
+                flags: int = 0) -> DecodeParams:
+    return DecodeParams(batch, num_q_heads, num_kv_heads, head_dim, page_size, sm_scale, out_dtype, chunk_pages,
+                        flags)
 
 
 # --------------------------------------------------------------------------- decode attention
@@ -191,8 +196,10 @@ def workspace_size(params: DecodeParams, max_total_pages: int) -> int:
 
 
 def alloc_workspace(params: DecodeParams, max_total_pages: int, device=None):
+    """Device workspace, zero-filled (the scheduler state and split counters must start at 0;
+    every call leaves them 0 again)."""
     import torch
-    return torch.empty(workspace_size(params, max_total_pages), dtype=torch.uint8,
+    return torch.zeros(workspace_size(params, max_total_pages), dtype=torch.uint8,
                        device=device if device is not None else "cuda")
 
 
@@ -234,9 +241,28 @@ def decode_attention(q, k_pages, v_pages, page_indptr, page_indices, kv_len, *, 
                           device=q.device)
     if lse is None and return_lse:
         lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device)
-    decode_plan(params, kv_len, page_indptr, total_pages, workspace, stream)
-    decode_run(params, q, k_pages, v_pages, page_indices, out, lse, workspace, stream)
+    attention_call(params, q, k_pages, v_pages, page_indptr, page_indices, kv_len, total_pages, out, lse,
+                   workspace, stream)
     return out, lse
+
+
+def attention_call(params: DecodeParams, q, k_pages, v_pages, page_indptr, page_indices, kv_len, total_pages: int,
+                   out, lse, workspace, stream=None):
+    """l4_decode_attention: plan + split-KV + combine in one launch (B <= 1024)."""
+    import torch
+    _need(q, torch.bfloat16, "q")
+    _need(k_pages, torch.bfloat16, "k_pages")
+    _need(v_pages, torch.bfloat16, "v_pages")
+    _need(page_indptr, torch.int32, "page_indptr")
+    _need(page_indices, torch.int32, "page_indices")
+    _need(kv_len, torch.int32, "kv_len")
+    _need(out, torch.float32 if params.out_dtype == L4_DT_F32 else torch.bfloat16, "out")
+    if lse is not None:
+        _need(lse, torch.float32, "lse")
+    _check(lib().l4_decode_attention(ctypes.byref(params), _ptr(q), _ptr(k_pages), _ptr(v_pages),
+                                     int(k_pages.shape[0]), _ptr(page_indptr), _ptr(page_indices), int(total_pages),
+                                     _ptr(kv_len), _ptr(out), _ptr(lse), _ptr(workspace), workspace.numel(),
+                                     _stream_handle(stream)))
 
 
 def plan_info(workspace, stream=None) -> PlanInfo:

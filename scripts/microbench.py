@@ -37,10 +37,18 @@ def main():
     plan = lambda: l4.decode_plan(p, wl.kv_len, wl.indptr, wl.table.total_pages, ws)
     run = lambda: l4.decode_run(p, wl.q, wl.k, wl.v, wl.indices, wl.out, wl.lse, ws)
     both = lambda: (plan(), run())
+    fused = lambda: l4.attention_call(p, wl.q, wl.k, wl.v, wl.indptr, wl.indices, wl.kv_len, wl.table.total_pages,
+                                      wl.out, wl.lse, ws)
+    pe = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, chunk_pages=args.chunk,
+                        flags=l4.L4_DECODE_EARLY_INPUTS)
+    early = lambda: l4.attention_call(pe, wl.q, wl.k, wl.v, wl.indptr, wl.indices, wl.kv_len, wl.table.total_pages,
+                                      wl.out, wl.lse, ws)
     plan()
     t_plan = timeit(plan)
     t_run = timeit(run)
     t_both = timeit(both)
+    t_fused = timeit(fused)
+    t_early = timeit(early)
     # device-only cost: the same calls captured in a CUDA graph (no host launch overhead)
     def graph_time(fn, reps=20):
         s = torch.cuda.Stream()
@@ -54,15 +62,20 @@ def main():
                     fn()
         return timeit(g.replay, iters=10, warm=2) / reps
     try:
-        g_plan, g_run, g_both = graph_time(plan), graph_time(run), graph_time(both)
+        g_plan, g_run, g_both, g_fused = graph_time(plan), graph_time(run), graph_time(both), graph_time(fused)
+        g_early = graph_time(early)
         print(f"  graph: plan {g_plan:.2f} us, run {g_run:.2f} us, plan+run {g_both:.2f} us "
-              f"({wl.bytes_kv / (g_both * 1e-6) / 1e9:.0f} GB/s)")
+              f"({wl.bytes_kv / (g_both * 1e-6) / 1e9:.0f} GB/s), fused {g_fused:.2f} us "
+              f"({wl.bytes_kv / (g_fused * 1e-6) / 1e9:.0f} GB/s), early {g_early:.2f} us "
+              f"({wl.bytes_kv / (g_early * 1e-6) / 1e9:.0f} GB/s)")
     except Exception as e:  # noqa
         print("  graph capture failed:", e)
     info = l4.plan_info(ws)
     gbs = wl.bytes_kv / (t_both * 1e-6) / 1e9
     print(f"{args.workload}: plan {t_plan:.2f} us, run {t_run:.2f} us ({wl.bytes_kv / (t_run * 1e-6) / 1e9:.0f} GB/s), "
-          f"plan+run {t_both:.2f} us ({gbs:.0f} GB/s); items {info.num_items} chunk {info.chunk_pages}")
+          f"plan+run {t_both:.2f} us ({gbs:.0f} GB/s), fused {t_fused:.2f} us "
+          f"({wl.bytes_kv / (t_fused * 1e-6) / 1e9:.0f} GB/s), early {t_early:.2f} us "
+          f"({wl.bytes_kv / (t_early * 1e-6) / 1e9:.0f} GB/s); items {info.num_items} chunk {info.chunk_pages}")
 
 
 if __name__ == "__main__":

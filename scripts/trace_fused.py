@@ -1,0 +1,55 @@
+"""Development timeline probe: run a trace build (L4_LIB=<variant .so built with -DL4_TRACE>)
+and print, over CTAs, when each phase of decode_kernel happened (us from the earliest start):
+0 entry, 1 after griddepcontrol.wait, 2 plan ready, 3 first TMA issued, 4 first page landed
+(consumer warp 0), 5 CTA done; inside the planner: 6 loads + reduction, 7 chunk/count,
+8 rank pass 1, 9 rank pass 2 (then offsets until 2)."""
+import argparse
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import bench
+from paper_2512_19179_b200 import l4
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--mode", default="fused", choices=["fused", "run"])
+    args = ap.parse_args()
+    spec = bench.WORKLOADS[args.workload]
+    wl = bench.Workload(args.workload, spec["lens"](), spec["shape"])
+    p = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads)
+    ws = l4.alloc_workspace(p, wl.table.total_pages)
+    l4.decode_plan(p, wl.kv_len, wl.indptr, wl.table.total_pages, ws)
+    if args.mode == "fused":
+        fn = lambda: l4.attention_call(p, wl.q, wl.k, wl.v, wl.indptr, wl.indices, wl.kv_len, wl.table.total_pages,
+                                       wl.out, wl.lse, ws)
+    else:
+        fn = lambda: l4.decode_run(p, wl.q, wl.k, wl.v, wl.indices, wl.out, wl.lse, ws)
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    fn()
+    b.record()
+    b.synchronize()
+    ncta = l4.plan_info(ws).num_ctas
+    buf = (ctypes.c_ulonglong * (4096 * 16))()
+    l4.lib().l4_trace_read(buf, 4096 * 16)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, :10].astype(np.float64)
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3
+    print(f"{args.workload} {args.mode}: event {a.elapsed_time(b) * 1e3:.1f} us, {ncta} CTAs")
+    for k, name in enumerate(["entry", "pdl_wait", "plan", "tma0", "land0", "done", "p_load", "p_count", "p_pass1", "p_pass2"]):
+        c = rel[:, k]
+        print(f"  {name:9s} min {c.min():8.2f}  p50 {np.median(c):8.2f}  p90 {np.percentile(c, 90):8.2f}  max {c.max():8.2f}")
+
+
+if __name__ == "__main__":
+    main()

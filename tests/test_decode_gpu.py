@@ -219,3 +219,91 @@ def test_full_size_c3_sampled():
 def test_full_size_c4_sampled():
     lens = synth.lengths_c4(0)
     _sampled_full_size(lens, synth.SHAPE_LLAMA3_70B, 0, [0, 31])
+
+
+# ----------------------------------------------------------------------------- fused single-launch path
+def _dev_case(lens, Hq, Hkv, seed):
+    shape, table, q, k, v, ro, rl = _case(lens, Hq, Hkv, seed=seed)
+    return (table, ro, rl) + _to_dev(table, q, k, v)
+
+
+def _plan_run(params, table, qd, kd, vd, ip, ix, kl, ws):
+    o = torch.empty(table.batch, params.num_q_heads, 128, device="cuda")
+    lz = torch.empty(table.batch, params.num_q_heads, device="cuda")
+    l4.decode_plan(params, kl, ip, table.total_pages, ws)
+    l4.decode_run(params, qd, kd, vd, ix, o, lz, ws)
+    return o, lz
+
+
+def _fused(params, table, qd, kd, vd, ip, ix, kl, ws):
+    o = torch.empty(table.batch, params.num_q_heads, 128, device="cuda")
+    lz = torch.empty(table.batch, params.num_q_heads, device="cuda")
+    l4.attention_call(params, qd, kd, vd, ip, ix, kl, table.total_pages, o, lz, ws)
+    return o, lz
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("chunk", [0, 2, -1])
+def test_fused_equals_plan_plus_run_bitwise(G, chunk):
+    """l4_decode_attention (one launch, per-CTA shared-memory plan) builds the same work list as
+    plan_kernel: outputs are bit-identical to l4_decode_plan + l4_decode_run, and match the oracle."""
+    rng = np.random.default_rng(7 * G + chunk)
+    lens = [0, 1, 16, 17, 255, 4000] + rng.integers(1, 2500, size=40).tolist() + [0]
+    Hkv = 2
+    table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, Hkv * G, Hkv, seed=G)
+    params = l4.make_params(table.batch, Hkv * G, Hkv, chunk_pages=chunk)
+    ws = l4.alloc_workspace(params, table.total_pages)
+    o1, l1 = _plan_run(params, table, qd, kd, vd, ip, ix, kl, ws)
+    o2, l2 = _fused(params, table, qd, kd, vd, ip, ix, kl, ws)
+    o3, l3 = _fused(params, table, qd, kd, vd, ip, ix, kl, ws)   # repeat: self-cleaning state
+    pe = l4.make_params(table.batch, Hkv * G, Hkv, chunk_pages=chunk, flags=l4.L4_DECODE_EARLY_INPUTS)
+    early = [_fused(pe, table, qd, kd, vd, ip, ix, kl, ws) for _ in range(3)]  # back to back (PDL overlap)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    assert torch.equal(o2, o3) and torch.equal(l2, l3)
+    for o4, l4_ in early:
+        assert torch.equal(o2, o4) and torch.equal(l2, l4_)
+    _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
+
+
+def test_fused_workspace_reuse_across_batch_sizes():
+    """One workspace, calls with different B (and split-heavy plans) back to back: the split
+    counters live in a region independent of B, so no call sees another call's stale items."""
+    p_max = l4.make_params(1024, 32, 8)
+    ws = None
+    for i, (B, hi) in enumerate([(3, 20000), (700, 3000), (5, 60000), (1024, 600), (1, 131072), (40, 9000)]):
+        rng = np.random.default_rng(50 + i)
+        lens = rng.integers(1, hi, size=B)
+        table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, 32, 8, seed=i)
+        if ws is None:
+            ws = l4.alloc_workspace(p_max, 200000)
+        params = l4.make_params(B, 32, 8)
+        if i % 2:
+            o, lz = _plan_run(params, table, qd, kd, vd, ip, ix, kl, ws)
+        else:
+            o, lz = _fused(params, table, qd, kd, vd, ip, ix, kl, ws)
+        torch.cuda.synchronize()
+        _check(o.double().cpu().numpy(), lz.double().cpu().numpy(), ro, rl)
+
+
+def test_fused_batch_limit_and_max_batch():
+    """B = 1024 (largest fused batch) and B = 8192 (largest batch, planner-kernel path) vs the oracle."""
+    for B, seed in ((1024, 1), (1025, 2), (8192, 3)):
+        rng = np.random.default_rng(seed)
+        lens = rng.integers(0, 40, size=B)
+        lens[rng.integers(0, B, size=4)] = [3000, 1, 0, 777]
+        table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, 8, 2, seed=seed)
+        out, lse = l4.decode_attention(qd, kd, vd, ip, ix, kl)
+        torch.cuda.synchronize()
+        _check(out.double().cpu().numpy(), lse.double().cpu().numpy(), ro, rl)
+
+
+def test_longest_request_split_cap():
+    """One 2^18-token request (16,384 pages) next to short ones: the split count is capped at
+    512 per (request, kv head), so the chunk grows past the automatic choice (8 -> 32 pages)."""
+    lens = [1 << 18, 3, 100]
+    table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, 8, 1, seed=11)
+    for chunk in (0, 1):
+        out, lse = l4.decode_attention(qd, kd, vd, ip, ix, kl, chunk_pages=chunk)
+        torch.cuda.synchronize()
+        _check(out.double().cpu().numpy(), lse.double().cpu().numpy(), ro, rl)

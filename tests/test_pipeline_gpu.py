@@ -26,6 +26,10 @@ class _Hub:
         self.mail = {}
         self.me = 0
 
+    @staticmethod
+    def get_backend():  # device tensors move as with NCCL (no host staging)
+        return "nccl"
+
     def isend(self):  # markers only
         pass
 
