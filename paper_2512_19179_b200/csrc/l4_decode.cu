@@ -241,7 +241,7 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
 }
 
 // Shared-memory scratch of plan_core (bytes; 8-byte aligned base).
-constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4;
+constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4;
 
 // The planner (a1), run by every thread of a CTA: reads kv_len / indptr, chooses the chunk C,
 // and orders the requests by length bin, longest bin first, request index ascending inside a
@@ -258,7 +258,8 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   long long* s_ll = reinterpret_cast<long long*>(scratch);
   int* s_i = reinterpret_cast<int*>(scratch + 32 * 8);
   unsigned* s_u = reinterpret_cast<unsigned*>(scratch + 32 * 8 + 36 * 4);
-  int* s_wcnt = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4);  // [nw][kNumBins]
+  int* s_w = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4);        // per-warp sums
+  int* s_wcnt = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4);  // [nw][kNumBins]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nw = nthr >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -316,10 +317,10 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-    if (lane == 0) s_i[warp] = wsum;
+    if (lane == 0) s_w[warp] = wsum;  // not s_i: slower warps may still read block_reduce3's s_i
     __syncthreads();
     N = 0;
-    for (int w = 0; w < nw; ++w) N += s_i[w];
+    for (int w = 0; w < nw; ++w) N += s_w[w];
     N *= Hkv;
     if (N <= items_cap || C >= INT_MAX / 8) break;
     C *= 2;
@@ -376,10 +377,10 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-    if (lane == 0) s_i[warp] = wsum;  // pass 1's counts in s_i were read two barriers ago
+    if (lane == 0) s_w[warp] = wsum;  // pass 1's counts in s_w were read two barriers ago
     __syncthreads();
     int carry = 0;
-    for (int w = 0; w < warp; ++w) carry += s_i[w];
+    for (int w = 0; w < warp; ++w) carry += s_w[w];
     carry *= Hkv;
     for (int t0 = r0; t0 < r1; t0 += 32) {
       const int r = t0 + lane;

@@ -48,6 +48,18 @@ def main():
     t_run = timeit(run)
     t_both = timeit(both)
     t_fused = timeit(fused)
+    def timeit_ev(fn, iters=50, warm=5):  # an event recorded after every call
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+        evs[0].record()
+        for i in range(iters):
+            fn()
+            evs[i + 1].record()
+        evs[-1].synchronize()
+        return evs[0].elapsed_time(evs[-1]) / iters * 1e3
+    print(f"  per-call events: fused {timeit_ev(fused):.2f} us, early {timeit_ev(early):.2f} us")
     t_early = timeit(early)
     # device-only cost: the same calls captured in a CUDA graph (no host launch overhead)
     def graph_time(fn, reps=20):

@@ -20,6 +20,18 @@ for G, Hkv, chunk in ((4, 2, 0), (8, 1, 2), (1, 3, -1)):
                                    chunk_pages=chunk)
     torch.cuda.synchronize()
     assert torch.isfinite(out).all()
+    # back-to-back single-launch calls with the early-input flag, then the two-launch path
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    ip, ix, kl = (torch.from_numpy(x).cuda() for x in (t.indptr, t.indices, t.kv_len))
+    pe = l4.make_params(len(lens), G * Hkv, Hkv, chunk_pages=chunk, flags=l4.L4_DECODE_EARLY_INPUTS)
+    ws = l4.alloc_workspace(pe, t.total_pages)
+    o2, l2 = torch.empty_like(out), torch.empty_like(lse)
+    for _ in range(3):
+        l4.attention_call(pe, qd, kd, vd, ip, ix, kl, t.total_pages, o2, l2, ws)
+    l4.decode_plan(pe, kl, ip, t.total_pages, ws)
+    l4.decode_run(pe, qd, kd, vd, ix, o2, l2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(o2, out)
 kk = torch.randn(2, 40, 2, 16, 128, device="cuda").to(torch.bfloat16)
 vv = torch.randn_like(kk)
 dk, dv = torch.zeros_like(kk), torch.zeros_like(vv)
