@@ -58,7 +58,8 @@ def main(tag="r1", wls=("c2", "c3", "c4")):
     os.makedirs(PROF, exist_ok=True)
     lines = [f"# ncu evidence — {tag}", "",
              "Captured under gpurun on one B200 with `scripts/gpu_round.sh` (`ncu --set full --clock-control none "
-             "--import-source on -k regex:decode_kernel`; launch lists with `--metrics gpu__time_duration.sum`). "
+             "--import-source on -k regex:<the single-launch decode_kernel<G, true>>`; launch lists with "
+             "`--metrics gpu__time_duration.sum`). "
              "ncu numbers are serialised, cold-cache replays: compare shares, not absolutes, with bench.py.", ""]
     for wl in wls:
         rep = os.path.join(OUT, f"prof_{tag}_{wl}.ncu-rep")
