@@ -57,10 +57,12 @@ constexpr int kItemSlots = 4;
 constexpr int kMaxG = 8;
 constexpr int kQSlotBytes = kMaxG * kHeadDim * 2;     // 2 KB
 constexpr int kMergeStride = kHeadDim + 4;            // floats per head row (bank-conflict padding)
-constexpr int kMaxSplits = 512;                       // per (request, kv head); lse staging capacity
+constexpr int kMaxSplits = 512;                       // per (request, kv head)
+constexpr int kCombineGroup = 16;                     // two-level combine: splits per group
+constexpr int kMaxCombine = kMaxSplits / kCombineGroup;  // partials read by one combine (>= group)
 constexpr int kMinChunk = 8;                          // pages
 #ifndef L4_ITEMS_PER_CTA
-#define L4_ITEMS_PER_CTA 8
+#define L4_ITEMS_PER_CTA 6
 #endif
 constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
@@ -100,7 +102,7 @@ static_assert(sizeof(PlanHeader) == 128, "PlanHeader is 128 bytes");
 
 // ------------------------------------------------------------------ workspace layout
 struct WsLayout {
-  size_t header, items, counters, part_lse, part_o, total;
+  size_t header, counters, gcount, items, part_lse, part_o, total;
   int items_cap;
 };
 
@@ -114,19 +116,21 @@ WsLayout ws_layout(int B, int Hkv, int G, int items_cap) {
   // counters are self-cleaning across runs, so their region must not depend on B: a workspace
   // reused with another batch size never sees stale items where its counters are
   (void)B;
-  L.items = align256(L.counters + (size_t)kMaxBatch * Hkv * sizeof(int));
+  L.gcount = align256(L.counters + (size_t)kMaxBatch * Hkv * sizeof(int));  // group counters, one per slot
+  L.items = align256(L.gcount + (size_t)items_cap * sizeof(int));
   L.part_lse = align256(L.items + (size_t)items_cap * sizeof(WorkItem));
   L.part_o = align256(L.part_lse + (size_t)items_cap * G * sizeof(float));
   L.total = align256(L.part_o + (size_t)items_cap * G * kHeadDim * sizeof(float));
   return L;
 }
 
-// The layout is a pure function of (B, Hkv, G, workspace_bytes): plan and run
+// The layout is a pure function of (Hkv, G, workspace_bytes): plan and run
 // both derive the largest item capacity that fits the caller's workspace.
 bool ws_layout_from_bytes(int B, int Hkv, int G, size_t bytes, WsLayout* out) {
   const WsLayout z = ws_layout(B, Hkv, G, 0);
   if (bytes < z.total) return false;
-  const size_t per_item = sizeof(WorkItem) + (size_t)G * sizeof(float) + (size_t)G * kHeadDim * sizeof(float);
+  const size_t per_item =
+      sizeof(int) + sizeof(WorkItem) + (size_t)G * sizeof(float) + (size_t)G * kHeadDim * sizeof(float);
   int64_t cap = (int64_t)((bytes - z.total) / per_item);
   cap = std::min<int64_t>(cap, INT_MAX / 64);
   while (cap > 0 && ws_layout(B, Hkv, G, (int)cap).total > bytes) --cap;
@@ -494,6 +498,7 @@ struct RunArgs {
   const WorkItem* items;
   PlanHeader* header;
   int* counters;
+  int* gcount;
   float* part_o;
   float* part_lse;
   int Hq, Hkv;
@@ -542,6 +547,124 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
   asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
+}
+
+// a3: log-sum-exp combine (FlashDecoding aggregation) of `cnt` partials held at
+// workspace slots slot0, slot0 + stride, ... (normalised O [G][128] and base-2 lse [G] each):
+//   M = max_s lse_s,  w_s = 2^(lse_s - M),  O = sum_s w_s O_s / sum_s w_s,  lse = M + log2 sum_s w_s.
+// The result goes to the output rows row0 .. row0 + G - 1 (to_output) or back to slot `dst` in
+// the same partial form (a group partial of the two-level combine).  Run by the 128 consumer
+// threads; float4 loads, up to 8 partials in flight per thread; fixed summation order.
+template <int G>
+__device__ __forceinline__ void combine_slots(const RunArgs& a, float* scratch, int slot0, int stride, int cnt,
+                                              bool to_output, size_t row0, int dst, int ct) {
+  using namespace dev;
+  const int warp = ct >> 5, lane = ct & 31;
+  float* s_w = scratch;                         // [cnt][G]: lse, then weights
+  float* s_M = scratch + kMaxCombine * kMaxG;   // [G]
+  float* s_L = s_M + kMaxG;                     // [G]
+  float4* s_acc = reinterpret_cast<float4*>(s_L + kMaxG);
+  for (int x = ct; x < cnt * G; x += kConsumerThreads) {
+    const int c = x / G, head = x - c * G;
+    s_w[x] = __ldcg(a.part_lse + (size_t)(slot0 + c * stride) * G + head);
+  }
+  named_bar_sync(1, kConsumerThreads);
+  for (int head = warp; head < G; head += kConsumerWarps) {
+    float m = -INFINITY;
+    for (int c = lane; c < cnt; c += 32) m = fmaxf(m, s_w[c * G + head]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float mu = (m == -INFINITY) ? 0.f : m;
+    float l = 0.f;
+    for (int c = lane; c < cnt; c += 32) {
+      const float w = ex2(s_w[c * G + head] - mu);
+      s_w[c * G + head] = w;
+      l += w;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) {
+      s_M[head] = m;
+      s_L[head] = l;
+    }
+  }
+  named_bar_sync(1, kConsumerThreads);
+  constexpr int F4 = G * (kHeadDim / 4);                  // float4 per partial
+  constexpr int kSpan = F4 < kConsumerThreads ? F4 : kConsumerThreads;
+  constexpr int kGroups = kConsumerThreads / kSpan;       // thread groups splitting the partials
+  constexpr int kPer = F4 / kSpan;                        // float4 per thread
+  const int f0 = ct % kSpan, grp = ct / kSpan;
+  float4 acc[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int c = grp;
+  for (; c + 7 * kGroups < cnt; c += 8 * kGroups) {
+    float4 v[8][kPer];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float4* src = reinterpret_cast<const float4*>(a.part_o + (size_t)(slot0 + (c + u * kGroups) * stride) * G * kHeadDim);
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) v[u][i] = __ldcg(src + f0 + i * kSpan);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const float w = s_w[(c + u * kGroups) * G + (f0 + i * kSpan) / 32];
+        acc[i].x += w * v[u][i].x;
+        acc[i].y += w * v[u][i].y;
+        acc[i].z += w * v[u][i].z;
+        acc[i].w += w * v[u][i].w;
+      }
+  }
+  for (; c < cnt; c += kGroups) {
+    const float4* src = reinterpret_cast<const float4*>(a.part_o + (size_t)(slot0 + c * stride) * G * kHeadDim);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const float4 v = __ldcg(src + f0 + i * kSpan);
+      const float w = s_w[c * G + (f0 + i * kSpan) / 32];
+      acc[i].x += w * v.x;
+      acc[i].y += w * v.y;
+      acc[i].z += w * v.z;
+      acc[i].w += w * v.w;
+    }
+  }
+  if constexpr (kGroups > 1) {  // fold the thread groups in a fixed order
+    s_acc[grp * kSpan + f0] = acc[0];
+    named_bar_sync(1, kConsumerThreads);
+    if (grp == 0) {
+      acc[0] = s_acc[f0];
+      for (int g2 = 1; g2 < kGroups; ++g2) {
+        const float4 t = s_acc[g2 * kSpan + f0];
+        acc[0].x += t.x;
+        acc[0].y += t.y;
+        acc[0].z += t.z;
+        acc[0].w += t.w;
+      }
+    }
+  }
+  if (grp != 0) return;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int f = f0 + i * kSpan, head = f / 32, d = (f % 32) * 4;
+    const float L = s_L[head], M = s_M[head];
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const float4 r = make_float4(acc[i].x * inv, acc[i].y * inv, acc[i].z * inv, acc[i].w * inv);
+    const float lse2 = L > 0.f ? M + __log2f(L) : -INFINITY;
+    if (to_output) {
+      const size_t row = row0 + head;
+      if (a.out_bf16) {
+        const uint32_t lo = pack_bf16(r.x, r.y), hi = pack_bf16(r.z, r.w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + row * kHeadDim + d) = make_uint2(lo, hi);
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + row * kHeadDim + d) = r;
+      }
+      if (d == 0 && a.lse) a.lse[row] = lse2 * kLn2;
+    } else {
+      *reinterpret_cast<float4*>(a.part_o + ((size_t)dst * G + head) * kHeadDim + d) = r;
+      if (d == 0) a.part_lse[(size_t)dst * G + head] = lse2;
+    }
+  }
 }
 
 // Byte offset of 16-B chunk cd (0..15) of token t in a staged slice: two
@@ -855,6 +978,44 @@ __global__ void __launch_bounds__(kThreads, 2)
   // ============================== consumer warps
   const int g = lane >> 2, c = lane & 3;
   const int ct = threadIdx.x;  // 0..127
+  // split bookkeeping for the deferred two-level combine (see the epilogue below)
+  auto group_need = [&](const WorkItem& w) -> int {
+    const int g0 = (w.split / kCombineGroup) * kCombineGroup;
+    return min(kCombineGroup, w.nsplit - g0);
+  };
+  auto group_ctr = [&](const WorkItem& w) -> int* {
+    if (w.nsplit > kCombineGroup) return a.gcount + w.part_base + (w.split / kCombineGroup) * kCombineGroup;
+    return a.counters + (size_t)w.b * a.Hkv + w.h;
+  };
+  auto finish_group = [&](const WorkItem& w) {  // this CTA was the last split of w's group
+#ifdef L4_TRACE
+    if (ct == 0) L4_MARK(10);
+#endif
+    const int ns = w.nsplit;
+    const int ng = (ns + kCombineGroup - 1) / kCombineGroup;
+    const int g0 = (w.split / kCombineGroup) * kCombineGroup;
+    const size_t row0 = (size_t)w.b * a.Hq + (size_t)w.h * G;
+    combine_slots<G>(a, merge_o, w.part_base + g0, 1, group_need(w), ng == 1, row0, w.part_base + g0, ct);
+    if (ng > 1) {
+      named_bar_sync(1, kConsumerThreads);
+      if (ct == 0) {
+        int* ctr = a.counters + (size_t)w.b * a.Hkv + w.h;
+        const int old = atom_add_acq_rel_gpu(ctr, 1);
+        const int last = (old == ng - 1);
+        if (last) *ctr = 0;
+        *s_flag = last;
+      }
+      named_bar_sync(1, kConsumerThreads);
+      if (*s_flag) combine_slots<G>(a, merge_o, w.part_base, kCombineGroup, ng, true, row0, 0, ct);
+    }
+#ifdef L4_TRACE
+    if (ct == 0) L4_MARK(11);
+#endif
+  };
+  bool has_pend = false;
+  WorkItem pend_it;
+  pend_it.b = -1;
+  int pend_old = 0;
   uint32_t qbase = 0;
   for (uint32_t k = 0;; ++k) {
     const uint32_t slot = k % kItemSlots;
@@ -961,57 +1122,37 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (d == 0) a.part_lse[prow] = lse2;
       }
     }
-    if (split) {
-      // ---- a3: the last split of (b, kv head) to finish combines all splits.
-      // Release: bar.sync orders every thread's partial stores before thread 0's
-      // acq_rel ticket (cumulative); acquire: the ticket, then bar.sync, then reads.
-      named_bar_sync(1, kConsumerThreads);
-      if (ct == 0) {
-        int* ctr = a.counters + (size_t)it.b * a.Hkv + it.h;
-        const int old = atom_add_acq_rel_gpu(ctr, 1);
-        const int last = (old == it.nsplit - 1);
-        if (last) *ctr = 0;  // self-cleaning: ready for the next run with the same plan
-        *s_flag = last;
-      }
-      named_bar_sync(1, kConsumerThreads);
-      if (*s_flag) {
-        float* s_lse = merge_o;  // reuse the merge area: [nsplit][G] base-2 lse
-        const int ns = it.nsplit;
-        for (int x = ct; x < ns * G; x += kConsumerThreads)
-          s_lse[x] = __ldcg(a.part_lse + (size_t)it.part_base * G + x);
-        named_bar_sync(1, kConsumerThreads);
-#pragma unroll
-        for (int o = ct; o < G * kHeadDim; o += kConsumerThreads) {
-          const int head = o / kHeadDim, d = o % kHeadDim;
-          float M = -INFINITY;
-          for (int s = 0; s < ns; ++s) M = fmaxf(M, s_lse[s * G + head]);
-          float sum = 0.f, L = 0.f;
-          const float* po = a.part_o + ((size_t)it.part_base * G + head) * kHeadDim + d;
-          int s = 0;
-          for (; s + 8 <= ns; s += 8) {
-            float v[8], w[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldcg(po + (size_t)(s + u) * G * kHeadDim);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) w[u] = ex2(s_lse[(s + u) * G + head] - M);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              sum += w[u] * v[u];
-              L += w[u];
-            }
-          }
-          for (; s < ns; ++s) {
-            const float w = ex2(s_lse[s * G + head] - M);
-            sum += w * __ldcg(po + (size_t)s * G * kHeadDim);
-            L += w;
-          }
-          const size_t row = (size_t)it.b * a.Hq + (size_t)it.h * G + head;
-          store_out(a, row * kHeadDim + d, sum / L);
-          if (d == 0 && a.lse) a.lse[row] = (M + __log2f(L)) * kLn2;
-        }
-      }
+    // ---- a3, two-level and deferred.  Split s belongs to group s / 16: the last split of a
+    // group to finish combines the group's partials into the group's first slot, and the last
+    // group of (b, kv head) to finish combines the group partials into the output; one combine
+    // reads at most 32 partials (<= 512 splits).  The group ticket of a split item is issued
+    // here but resolved at the end of this CTA's NEXT item, so no consumer waits for an atomic
+    // round trip between items.  Counters are self-cleaning (reset by the last arrival).
+    // Release: bar.sync orders every thread's partial stores before thread 0's acq_rel ticket
+    // (cumulative); acquire: the ticket, then bar.sync, then ld.global.cg reads.
+    named_bar_sync(1, kConsumerThreads);
+    if (has_pend && ct == 0) {
+      const int last = (pend_old == group_need(pend_it) - 1);
+      if (last) *group_ctr(pend_it) = 0;
+      *s_flag = last;
     }
+    if (split && ct == 0) pend_old = atom_add_acq_rel_gpu(group_ctr(it), 1);
+    if (has_pend) {
+      named_bar_sync(1, kConsumerThreads);
+      if (*s_flag) finish_group(pend_it);
+    }
+    has_pend = split;
+    if (split) pend_it = it;
     named_bar_sync(1, kConsumerThreads);  // merge area free for the next item
+  }
+  if (has_pend) {  // the last split item's ticket
+    if (ct == 0) {
+      const int last = (pend_old == group_need(pend_it) - 1);
+      if (last) *group_ctr(pend_it) = 0;
+      *s_flag = last;
+    }
+    named_bar_sync(1, kConsumerThreads);
+    if (*s_flag) finish_group(pend_it);
   }
   if (threadIdx.x == 0) L4_MARK(5);
 }
@@ -1142,6 +1283,10 @@ extern "C" size_t l4_decode_workspace_size(const l4_decode_params* p, int64_t ma
 extern "C" int l4_trace_read(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (size_t)n);
 }
+extern "C" int l4_trace_clear(void) {
+  static unsigned long long zeros[4096 * 16];
+  return (int)cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros));
+}
 #endif
 
 extern "C" l4_status l4_decode_workspace_init(const l4_decode_params* p, void* workspace, size_t workspace_bytes,
@@ -1150,8 +1295,10 @@ extern "C" l4_status l4_decode_workspace_init(const l4_decode_params* p, void* w
   l4_status s = check_params(p, &G);
   if (s != L4_OK) return s;
   if (!workspace) return fail(L4_ERR_WORKSPACE, "workspace is NULL");
-  const size_t head = ws_layout(p->batch, p->num_kv_heads, G, 0).items;  // header + split counters
-  if (workspace_bytes < head) return fail(L4_ERR_WORKSPACE, "workspace too small");
+  WsLayout L;
+  if (!ws_layout_from_bytes(p->batch, p->num_kv_heads, G, workspace_bytes, &L))
+    return fail(L4_ERR_WORKSPACE, "workspace too small");
+  const size_t head = L.items;  // header + split counters + group counters
   cudaError_t e = cudaMemsetAsync(workspace, 0, head, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     set_error("cudaMemsetAsync: %s", cudaGetErrorString(e));
@@ -1256,6 +1403,7 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   a.items = reinterpret_cast<const WorkItem*>(ws + L.items);
   a.header = reinterpret_cast<PlanHeader*>(ws + L.header);
   a.counters = reinterpret_cast<int*>(ws + L.counters);
+  a.gcount = reinterpret_cast<int*>(ws + L.gcount);
   a.part_o = reinterpret_cast<float*>(ws + L.part_o);
   a.part_lse = reinterpret_cast<float*>(ws + L.part_lse);
   a.Hq = p->num_q_heads;
@@ -1344,7 +1492,8 @@ extern "C" l4_status l4_decode_plan_items(const void* workspace, int32_t* items_
   cudaError_t e = cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess) {
-    const size_t items_off = align256(256 + (size_t)kMaxBatch * h.num_kv_heads * sizeof(int));
+    const size_t gcount_off = align256(256 + (size_t)kMaxBatch * h.num_kv_heads * sizeof(int));
+    const size_t items_off = align256(gcount_off + (size_t)h.items_cap * sizeof(int));
     const int n = std::min(h.n_items, max_items);
     if (n > 0)
       e = cudaMemcpyAsync(items_out, static_cast<const char*>(workspace) + items_off, (size_t)n * sizeof(WorkItem),

@@ -29,9 +29,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--bin", type=int, nargs=2, default=None, help="only the workload's requests in [lo, hi)")
+    ap.add_argument("--quick", action="store_true", help="fused / early only")
     args = ap.parse_args()
     spec = bench.WORKLOADS[args.workload]
-    wl = bench.Workload(args.workload, spec["lens"](), spec["shape"])
+    lens = spec["lens"]()
+    if args.bin:
+        lens = lens[(lens >= args.bin[0]) & (lens < args.bin[1])]
+    wl = bench.Workload(args.workload, lens, spec["shape"])
     p = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, chunk_pages=args.chunk)
     ws = l4.alloc_workspace(p, wl.table.total_pages)
     plan = lambda: l4.decode_plan(p, wl.kv_len, wl.indptr, wl.table.total_pages, ws)
@@ -44,6 +49,12 @@ def main():
     early = lambda: l4.attention_call(pe, wl.q, wl.k, wl.v, wl.indptr, wl.indices, wl.kv_len, wl.table.total_pages,
                                       wl.out, wl.lse, ws)
     plan()
+    if args.quick:
+        t_fused, t_early = timeit(fused), timeit(early)
+        print(f"{args.workload} {args.bin or ''} {os.environ.get('L4_LIB', 'libl4.so')}: fused {t_fused:.2f} us "
+              f"({wl.bytes_kv / (t_fused * 1e-6) / 1e9:.0f} GB/s), early {t_early:.2f} us "
+              f"({wl.bytes_kv / (t_early * 1e-6) / 1e9:.0f} GB/s)")
+        return
     t_plan = timeit(plan)
     t_run = timeit(run)
     t_both = timeit(both)

@@ -19,14 +19,19 @@ from paper_2512_19179_b200 import l4
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
-    ap.add_argument("--mode", default="fused", choices=["fused", "run"])
+    ap.add_argument("--mode", default="fused", choices=["fused", "run", "early"])
+    ap.add_argument("--bin", type=int, nargs=2, default=None, help="only the workload's requests in [lo, hi)")
     args = ap.parse_args()
     spec = bench.WORKLOADS[args.workload]
-    wl = bench.Workload(args.workload, spec["lens"](), spec["shape"])
-    p = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads)
+    lens = spec["lens"]()
+    if args.bin:
+        lens = lens[(lens >= args.bin[0]) & (lens < args.bin[1])]
+    wl = bench.Workload(args.workload, lens, spec["shape"])
+    flags = l4.L4_DECODE_EARLY_INPUTS if args.mode == "early" else 0
+    p = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, flags=flags)
     ws = l4.alloc_workspace(p, wl.table.total_pages)
     l4.decode_plan(p, wl.kv_len, wl.indptr, wl.table.total_pages, ws)
-    if args.mode == "fused":
+    if args.mode in ("fused", "early"):
         fn = lambda: l4.attention_call(p, wl.q, wl.k, wl.v, wl.indptr, wl.indices, wl.kv_len, wl.table.total_pages,
                                        wl.out, wl.lse, ws)
     else:
@@ -40,14 +45,22 @@ def main():
     b.record()
     b.synchronize()
     ncta = l4.plan_info(ws).num_ctas
+    l4.lib().l4_trace_clear()
+    fn()
+    torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (4096 * 16))()
     l4.lib().l4_trace_read(buf, 4096 * 16)
-    t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, :10].astype(np.float64)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, :12].astype(np.float64)
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
-    print(f"{args.workload} {args.mode}: event {a.elapsed_time(b) * 1e3:.1f} us, {ncta} CTAs")
-    for k, name in enumerate(["entry", "pdl_wait", "plan", "tma0", "land0", "done", "p_load", "p_count", "p_pass1", "p_pass2"]):
+    bytes_kv = wl.bytes_kv
+    print(f"{args.workload} {args.bin} {args.mode}: {bytes_kv / 1e6:.0f} MB KV, event {a.elapsed_time(b) * 1e3:.1f} us, {ncta} CTAs")
+    for k, name in enumerate(["entry", "pdl_wait", "plan", "tma0", "land0", "done", "p_load", "p_count", "p_pass1", "p_pass2",
+                                   "comb_beg", "comb_end"]):
         c = rel[:, k]
+        c = c[(c > -1e6) & (c < 1e7)]  # marks a CTA never reached hold stale values
+        if c.size == 0:
+            continue
         print(f"  {name:9s} min {c.min():8.2f}  p50 {np.median(c):8.2f}  p90 {np.percentile(c, 90):8.2f}  max {c.max():8.2f}")
 
 
