@@ -307,3 +307,19 @@ def test_longest_request_split_cap():
         out, lse = l4.decode_attention(qd, kd, vd, ip, ix, kl, chunk_pages=chunk)
         torch.cuda.synchronize()
         _check(out.double().cpu().numpy(), lse.double().cpu().numpy(), ro, rl)
+
+
+@pytest.mark.parametrize("G", [1, 2, 8])
+def test_two_level_combine_group_boundaries(G):
+    """chunk_pages=1 splits a request of p > 2 pages p ways: split counts around the 16-split
+    group size (15, 16, 17, 31, 32, 33), a many-group request (200) and the 512-split cap
+    exercise both combine levels and ragged last groups; fp32 and bf16 outputs."""
+    ns_list = [2, 3, 15, 16, 17, 31, 32, 33, 200, 512]
+    lens = [16 * n - 5 for n in ns_list] + [0, 7]
+    Hkv = 2
+    shape, table, q, k, v, ro, rl = _case(lens, Hkv * G, Hkv, seed=20 + G)
+    out, lse = _run_gpu(table, q, k, v, chunk_pages=1)
+    _check(out, lse, ro, rl)
+    ob, lb = _run_gpu(table, q, k, v, chunk_pages=1, out_dtype=l4.L4_DT_BF16)
+    assert np.max(np.abs(ob - ro) - np.abs(ro) * 2.0 ** -8) <= TOL
+    _check(ob * 0, lb, ro * 0, rl)
