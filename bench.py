@@ -384,11 +384,13 @@ def heterogeneity_slowdown(steps: int, warmup: int):
     return out
 
 
-def migration_bandwidth(reps: int = 5):
+def migration_bandwidth(reps: int = 10):
     """l4_migrate of one request at the Llama-3-8B shape with all 32 layers:
     a 2048-token request = 128 pages x 32 layers x (K, V) = 256 MiB.  Loopback on one GPU
     (HBM -> HBM: every byte read and written once); over NVLink the same kernel writes to
-    IPC-mapped peer pools."""
+    IPC-mapped peer pools.  Reported: the copy kernel alone (l4_copy_pages, `reps` launches
+    between one event pair), the whole l4_migrate call (host allocation + launch, per call),
+    and torch's device copy of the same byte count as the loopback reference."""
     import torch
     from paper_2512_19179_b200 import l4
     layers, pages, n = 32, 2048, 128
@@ -397,7 +399,22 @@ def migration_bandwidth(reps: int = 5):
     k2, v2 = torch.empty_like(k), torch.empty_like(v)
     src, dst = l4.kv_view(k, v, num_layers=layers), l4.kv_view(k2, v2, num_layers=layers)
     sp = np.random.default_rng(0).permutation(pages)[:n]
+    dp = np.random.default_rng(1).permutation(pages)[:n]
     nbytes = n * layers * 2 * src.page_bytes
+
+    def timed(fn, r):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(r):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / r
+
+    t_kernel = timed(lambda: l4.copy_pages(src, sp, dst, dp), reps)
     times = []
     for i in range(reps + 2):
         pool = l4.PagePool(pages)
@@ -408,12 +425,18 @@ def migration_bandwidth(reps: int = 5):
         e1.synchronize()
         if i >= 2:
             times.append(e0.elapsed_time(e1))
-    t = float(np.median(times))
-    del k, v, k2, v2
+    t_call = float(np.median(times))
+    a_ = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    b_ = torch.empty_like(a_)
+    t_torch = timed(lambda: b_.copy_(a_), reps)
+    del k, v, k2, v2, a_, b_
     torch.cuda.empty_cache()
-    return dict(request_tokens=n * 16, layers=layers, bytes=int(nbytes), ms=round(t, 4),
-                gbs_moved=round(nbytes / (t / 1e3) / 1e9, 1), gbs_hbm_traffic=round(2 * nbytes / (t / 1e3) / 1e9, 1),
-                note="loopback src->dst on one GPU; HBM traffic = read + write")
+    return dict(request_tokens=n * 16, layers=layers, bytes=int(nbytes),
+                kernel_ms=round(t_kernel, 4), kernel_gbs_moved=round(nbytes / (t_kernel / 1e3) / 1e9, 1),
+                kernel_gbs_hbm_traffic=round(2 * nbytes / (t_kernel / 1e3) / 1e9, 1),
+                call_ms=round(t_call, 4), call_gbs_moved=round(nbytes / (t_call / 1e3) / 1e9, 1),
+                torch_copy_same_bytes_ms=round(t_torch, 4),
+                note="loopback src->dst on one GPU; HBM traffic = read + write; 4096 32 KB slices")
 
 
 # ----------------------------------------------------------------------------- pipeline (N > 1)
