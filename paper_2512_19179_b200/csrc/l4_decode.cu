@@ -49,13 +49,11 @@ constexpr int kHeadDim = 128;
 constexpr int kConsumerWarps = 4;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kThreads = kConsumerThreads + 32;      // + 1 producer warp = 160
-constexpr int kStages = 8;
 constexpr int kSliceBytes = kPage * kHeadDim * 2;     // one (page, kv head) K or V slice = 4 KB
 constexpr int kHalfBytes = kSliceBytes / 2;           // 16 rows x 64 bf16 (128 B swizzle span)
 constexpr int kStageBytes = 2 * kSliceBytes;          // K, V
 constexpr int kItemSlots = 4;
 constexpr int kMaxG = 8;
-constexpr int kQSlotBytes = kMaxG * kHeadDim * 2;     // 2 KB
 constexpr int kMergeStride = kHeadDim + 4;            // floats per head row (bank-conflict padding)
 constexpr int kMaxSplits = 512;                       // per (request, kv head)
 constexpr int kCombineGroup = 16;                     // two-level combine: splits per group
@@ -87,6 +85,13 @@ __device__ __forceinline__ void trace_mark(int k) {
   g_trace[blockIdx.x * 16 + k] = t;
 }
 #define L4_MARK(k) trace_mark(k)
+__device__ __forceinline__ unsigned long long trace_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// accumulated per-CTA counters in slots 12..15 (consumer warp 0 / producer lane 0)
+__device__ __forceinline__ void trace_add(int k, unsigned long long v) { g_trace[blockIdx.x * 16 + k] += v; }
 #else
 #define L4_MARK(k) ((void)0)
 #endif
@@ -516,25 +521,42 @@ struct __align__(16) SlotItem {  // item handed from the producer to the consume
   int idx, pad[3];
 };
 
+constexpr int kCombineScratchBytes = (kMaxCombine * kMaxG + 2 * kMaxG) * 4 + kConsumerThreads * 16;
+constexpr int cmax(int x, int y) { return x > y ? x : y; }
+constexpr int align16c(int x) { return (x + 15) & ~15; }
+
+// Shared memory of decode_kernel<G>, sized for its GQA group (Q slots of G rows, a warp merge
+// area of G heads that doubles as planner / combine scratch).  The page ring has 8 stages for
+// every G.  Its depth must stay a multiple of the 4 consumer warps: pages go to warps
+// round-robin inside an item, so the previous use of a stage (page q - 8) was consumed by the
+// same warp (or before the item barrier) and has completed; with, e.g., 10 stages page q - 10
+// belongs to another warp, may still be in flight, and a parity-only wait on its stage would
+// return early on the older phase (measured: 9 and 10 stages fail at full size).
+template <int G>
 struct SmemLayout {
+  static constexpr int stages_n = 8;
+  static_assert(stages_n % kConsumerWarps == 0, "stage parity waits need stages % consumer warps == 0");
+  static constexpr int qslot_bytes = G * kHeadDim * 2;
+  static constexpr int merge_bytes =
+      align16c(cmax(kConsumerWarps * G * kMergeStride * 4, cmax(kPlanScratchBytes, kCombineScratchBytes)));
   static constexpr int stages = 0;
-  static constexpr int qslots = stages + kStages * kStageBytes;
-  static constexpr int items = qslots + kItemSlots * kQSlotBytes;
+  static constexpr int qslots = stages + stages_n * kStageBytes;
+  static constexpr int items = align16c(qslots + kItemSlots * qslot_bytes);
   static constexpr int merge_o = items + kItemSlots * (int)sizeof(SlotItem);
-  static constexpr int merge_m = merge_o + kConsumerWarps * kMaxG * kMergeStride * 4;
+  static constexpr int merge_m = merge_o + merge_bytes;
   static constexpr int merge_l = merge_m + kConsumerWarps * kMaxG * 4;
   static constexpr int bars = merge_l + kConsumerWarps * kMaxG * 4;
-  static constexpr int nbars = 2 * kStages + 2 * kItemSlots;
+  static constexpr int nbars = 2 * stages_n + 2 * kItemSlots;
   static constexpr int flag = bars + nbars * 8;
-  static constexpr int total = flag + 16;
+  static constexpr int total = align16c(flag + 16);
   static constexpr int alloc = total + 1024;  // room to align the base to 1024 B (128B swizzle)
+  static_assert(merge_o % 16 == 0 && total % 16 == 0 && bars % 8 == 0, "aligned areas");
 };
-static_assert(kMaxSplits * kMaxG * 4 <= kConsumerWarps * kMaxG * kMergeStride * 4, "lse staging fits merge area");
-static_assert(kPlanScratchBytes <= kConsumerWarps * kMaxG * kMergeStride * 4, "plan scratch fits merge area");
-static_assert(SmemLayout::merge_o % 8 == 0 && SmemLayout::total % 16 == 0, "plan areas aligned");
 // Fused path: plan arrays s_len, s_ptr, s_rb [B] and s_off [B+1] after the kernel's own layout.
 inline size_t fused_plan_bytes(int B) { return ((size_t)(4 * B + 1) * 4 + 15) & ~size_t(15); }
-constexpr int kFusedMaxBatch = 1024;  // 2 CTAs per SM still fit (2 x ~108 KB)
+constexpr int kFusedMaxBatch = 1024;  // 2 CTAs per SM still fit (2 x <= 111 KB)
+static_assert(2 * (SmemLayout<4>::alloc + (4 * kFusedMaxBatch + 1) * 4 + 16 + 1024) <= 228 * 1024, "2 CTAs/SM (G=4)");
+static_assert(2 * (SmemLayout<8>::alloc + (4 * kFusedMaxBatch + 1) * 4 + 16 + 1024) <= 228 * 1024, "2 CTAs/SM (G=8)");
 
 __device__ __forceinline__ void store_out(const RunArgs& a, size_t idx, float v) {
   if (a.out_bf16)
@@ -766,19 +788,21 @@ template <int G, bool kFused>
 __global__ void __launch_bounds__(kThreads, 2)
     decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, RunArgs a) {
   using namespace dev;
+  using SL = SmemLayout<G>;
+  constexpr int kStages = SL::stages_n;
   extern __shared__ unsigned char smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   unsigned char* smem = smem_raw + ((1024u - (raw_u32 & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_full = sbase + SmemLayout::bars;
+  const uint32_t bar_full = sbase + SL::bars;
   const uint32_t bar_empty = bar_full + kStages * 8;
   const uint32_t bar_ifull = bar_empty + kStages * 8;
   const uint32_t bar_iempty = bar_ifull + kItemSlots * 8;
-  SlotItem* s_items = reinterpret_cast<SlotItem*>(smem + SmemLayout::items);
-  float* merge_o = reinterpret_cast<float*>(smem + SmemLayout::merge_o);
-  float* merge_m = reinterpret_cast<float*>(smem + SmemLayout::merge_m);
-  float* merge_l = reinterpret_cast<float*>(smem + SmemLayout::merge_l);
-  volatile int* s_flag = reinterpret_cast<volatile int*>(smem + SmemLayout::flag);
+  SlotItem* s_items = reinterpret_cast<SlotItem*>(smem + SL::items);
+  float* merge_o = reinterpret_cast<float*>(smem + SL::merge_o);
+  float* merge_m = reinterpret_cast<float*>(smem + SL::merge_m);
+  float* merge_l = reinterpret_cast<float*>(smem + SL::merge_l);
+  volatile int* s_flag = reinterpret_cast<volatile int*>(smem + SL::flag);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) L4_MARK(0);
@@ -822,13 +846,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   if constexpr (kFused) {
     // a1 in every CTA: the plan lives in this CTA's shared memory (scratch in the merge area,
     // free until the first item finishes); no planner launch and no global work list.
-    p_len = reinterpret_cast<int*>(smem + SmemLayout::total);
+    p_len = reinterpret_cast<int*>(smem + SL::total);
     p_ptr = p_len + a.B;
     p_rb = p_ptr + a.B;
     p_off = p_rb + a.B;
     int pmax;
     plan_core(a.kv_len, a.indptr, a.B, a.Hkv, W, a.forced_chunk, a.items_cap, p_len, p_ptr, p_rb, p_off,
-              smem + SmemLayout::merge_o, &plan_C, &n_items, &pmax);
+              smem + SL::merge_o, &plan_C, &n_items, &pmax);
   } else {
     n_items = a.header->n_items;
   }
@@ -873,17 +897,23 @@ __global__ void __launch_bounds__(kThreads, 2)
       s_items[slot] = si;
       const uint32_t qbytes = G * kHeadDim * 2;
       mbar_arrive_expect_tx(bar_ifull + slot * 8, qbytes);
-      bulk_load(sbase + SmemLayout::qslots + slot * kQSlotBytes,
+      bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes,
                 a.q + ((size_t)it.b * a.Hq + (size_t)it.h * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
     };
     uint32_t qseq = 0;
     auto issue_page = [&](int page, int h) {  // lane 0: one (page, kv head) K + V slice
       const uint32_t st = qseq % kStages;
+#ifdef L4_TRACE
+      const unsigned long long tw0 = trace_now();
+#endif
       mbar_wait(bar_empty + st * 8, ((qseq / kStages) & 1) ^ 1);
+#ifdef L4_TRACE
+      trace_add(14, trace_now() - tw0);
+#endif
       const uint32_t fb = bar_full + st * 8;
       mbar_arrive_expect_tx(fb, kStageBytes);
       const int row = (page * a.Hkv + h) * kPage;
-      const uint32_t dst = sbase + SmemLayout::stages + st * kStageBytes;
+      const uint32_t dst = sbase + SL::stages + st * kStageBytes;
       tma_load_3d(dst, &tmK, 0, row, 0, fb, policy);
       tma_load_3d(dst + kSliceBytes, &tmV, 0, row, 0, fb, policy);
 #ifdef L4_TRACE
@@ -1025,7 +1055,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (it.b < 0) break;
     uint32_t qf[8][2];
     {
-      const unsigned char* qs = smem + SmemLayout::qslots + slot * kQSlotBytes;
+      const unsigned char* qs = smem + SL::qslots + slot * SL::qslot_bytes;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         if (g < G) {
@@ -1048,17 +1078,24 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int j = warp; j < np; j += kConsumerWarps) {
       const uint32_t q = qbase + j;
       const uint32_t st = q % kStages;
+#ifdef L4_TRACE
+      const unsigned long long tw0 = trace_now();
+#endif
       mbar_wait(bar_full + st * 8, (q / kStages) & 1);
 #ifdef L4_TRACE
       if (q == 0 && lane == 0) L4_MARK(4);
+      if (warp == 0 && lane == 0) trace_add(12, trace_now() - tw0);
 #endif
       const int valid = (j == np - 1) ? it.last_valid : kPage;
-      consume_page(sbase + SmemLayout::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane);
+      consume_page(sbase + SL::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + st * 8);
     }
     qbase += np;
     if (early && k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
+#ifdef L4_TRACE
+    const unsigned long long te0 = trace_now();
+#endif
 
     // ---- intra-CTA merge of the 4 warps' (m, l, O)
 #pragma unroll
@@ -1067,7 +1104,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       lrow[1] += __shfl_xor_sync(0xffffffffu, lrow[1], o);
     }
     {
-      float* mo = merge_o + warp * (kMaxG * kMergeStride);
+      float* mo = merge_o + warp * (G * kMergeStride);
       const int h0 = 2 * c, h1 = 2 * c + 1;
       if (h0 < G) {
 #pragma unroll
@@ -1106,7 +1143,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) {
           const float sc = ex2(merge_m[w * kMaxG + head] - M);
-          sum += sc * merge_o[w * (kMaxG * kMergeStride) + head * kMergeStride + d];
+          sum += sc * merge_o[w * (G * kMergeStride) + head * kMergeStride + d];
           L += sc * merge_l[w * kMaxG + head];
         }
         val = sum / L;
@@ -1144,6 +1181,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     has_pend = split;
     if (split) pend_it = it;
     named_bar_sync(1, kConsumerThreads);  // merge area free for the next item
+#ifdef L4_TRACE
+    if (ct == 0) {
+      trace_add(13, trace_now() - te0);
+      trace_add(15, 1);
+    }
+#endif
   }
   if (has_pend) {  // the last split item's ticket
     if (ct == 0) {
@@ -1198,7 +1241,7 @@ l4_status make_tmap(CUtensorMap* tm, const void* base, int64_t rows) {
 template <int G, bool kFused>
 l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunArgs& a, int grid, cudaStream_t st) {
   static bool attr_set[64] = {false};
-  const size_t smem_max = SmemLayout::alloc + (kFused ? fused_plan_bytes(kFusedMaxBatch) : 0);
+  const size_t smem_max = SmemLayout<G>::alloc + (kFused ? fused_plan_bytes(kFusedMaxBatch) : 0);
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_set[dev]) {
@@ -1217,7 +1260,7 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunA
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = SmemLayout::alloc + (kFused ? fused_plan_bytes(a.B) : 0);
+  cfg.dynamicSmemBytes = SmemLayout<G>::alloc + (kFused ? fused_plan_bytes(a.B) : 0);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: overlap with the previous kernel

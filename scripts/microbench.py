@@ -31,11 +31,18 @@ def main():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--bin", type=int, nargs=2, default=None, help="only the workload's requests in [lo, hi)")
     ap.add_argument("--quick", action="store_true", help="fused / early only")
+    ap.add_argument("--fig2", type=int, nargs=3, default=None, help="short long n_long: Fig. 2 batch of 512")
+    ap.add_argument("--uniform", type=int, nargs=2, default=None, help="batch length: homogeneous batch")
     args = ap.parse_args()
     spec = bench.WORKLOADS[args.workload]
     lens = spec["lens"]()
     if args.bin:
         lens = lens[(lens >= args.bin[0]) & (lens < args.bin[1])]
+    if args.fig2:
+        import synth
+        lens = synth.lengths_fig2(512, args.fig2[2], args.fig2[0], args.fig2[1])
+    if args.uniform:
+        lens = np.full(args.uniform[0], args.uniform[1], dtype=np.int64)
     wl = bench.Workload(args.workload, lens, spec["shape"])
     p = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, chunk_pages=args.chunk)
     ws = l4.alloc_workspace(p, wl.table.total_pages)
@@ -51,7 +58,7 @@ def main():
     plan()
     if args.quick:
         t_fused, t_early = timeit(fused), timeit(early)
-        print(f"{args.workload} {args.bin or ''} {os.environ.get('L4_LIB', 'libl4.so')}: fused {t_fused:.2f} us "
+        print(f"{args.workload} {args.bin or args.fig2 or args.uniform or ''} {os.environ.get('L4_LIB', 'libl4.so')}: fused {t_fused:.2f} us "
               f"({wl.bytes_kv / (t_fused * 1e-6) / 1e9:.0f} GB/s), early {t_early:.2f} us "
               f"({wl.bytes_kv / (t_early * 1e-6) / 1e9:.0f} GB/s)")
         return

@@ -21,11 +21,18 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--mode", default="fused", choices=["fused", "run", "early"])
     ap.add_argument("--bin", type=int, nargs=2, default=None, help="only the workload's requests in [lo, hi)")
+    ap.add_argument("--fig2", type=int, nargs=3, default=None, help="short long n_long: Fig. 2 batch of 512")
+    ap.add_argument("--uniform", type=int, nargs=2, default=None, help="batch length: homogeneous batch")
     args = ap.parse_args()
     spec = bench.WORKLOADS[args.workload]
     lens = spec["lens"]()
     if args.bin:
         lens = lens[(lens >= args.bin[0]) & (lens < args.bin[1])]
+    if args.fig2:
+        import synth
+        lens = synth.lengths_fig2(512, args.fig2[2], args.fig2[0], args.fig2[1])
+    if args.uniform:
+        lens = np.full(args.uniform[0], args.uniform[1], dtype=np.int64)
     wl = bench.Workload(args.workload, lens, spec["shape"])
     flags = l4.L4_DECODE_EARLY_INPUTS if args.mode == "early" else 0
     p = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, flags=flags)
@@ -55,6 +62,12 @@ def main():
     rel = (t - t0) / 1e3
     bytes_kv = wl.bytes_kv
     print(f"{args.workload} {args.bin} {args.mode}: {bytes_kv / 1e6:.0f} MB KV, event {a.elapsed_time(b) * 1e3:.1f} us, {ncta} CTAs")
+    acc = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, 12:16].astype(np.float64)
+    span = (t[:, 5] - t[:, 0]) / 1e3
+    print(f"  per CTA (us, median over CTAs): busy {np.median(span):.1f}; consumer warp0 waiting for data "
+          f"{np.median(acc[:, 0]) / 1e3:.1f}; item epilogues {np.median(acc[:, 1]) / 1e3:.1f}; producer waiting "
+          f"for ring slots {np.median(acc[:, 2]) / 1e3:.1f}; items {np.median(acc[:, 3]):.0f} "
+          f"(min {acc[:, 3].min():.0f}, max {acc[:, 3].max():.0f})")
     for k, name in enumerate(["entry", "pdl_wait", "plan", "tma0", "land0", "done", "p_load", "p_count", "p_pass1", "p_pass2",
                                    "comb_beg", "comb_end"]):
         c = rel[:, k]
