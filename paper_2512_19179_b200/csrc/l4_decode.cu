@@ -91,7 +91,10 @@ __device__ __forceinline__ unsigned long long trace_now() {
   return t;
 }
 // accumulated per-CTA counters in slots 12..15 (consumer warp 0 / producer lane 0)
-__device__ __forceinline__ void trace_add(int k, unsigned long long v) { g_trace[blockIdx.x * 16 + k] += v; }
+// accumulated in a per-thread register array (tr_acc), stored once when the thread finishes
+#define L4_TRACE_ACC unsigned long long tr_acc[16] = {0};
+#define trace_add(k, v) (tr_acc[(k)] += (v))
+#define L4_TRACE_FLUSH(k) (g_trace[blockIdx.x * 16 + (k)] = tr_acc[(k)])
 #else
 #define L4_MARK(k) ((void)0)
 #endif
@@ -526,16 +529,21 @@ constexpr int cmax(int x, int y) { return x > y ? x : y; }
 constexpr int align16c(int x) { return (x + 15) & ~15; }
 
 // Shared memory of decode_kernel<G>, sized for its GQA group (Q slots of G rows, a warp merge
-// area of G heads that doubles as planner / combine scratch).  The page ring has 8 stages for
-// every G.  Its depth must stay a multiple of the 4 consumer warps: pages go to warps
-// round-robin inside an item, so the previous use of a stage (page q - 8) was consumed by the
-// same warp (or before the item barrier) and has completed; with, e.g., 10 stages page q - 10
-// belongs to another warp, may still be in flight, and a parity-only wait on its stage would
-// return early on the older phase (measured: 9 and 10 stages fail at full size).
+// area of G heads that doubles as planner / combine scratch).  The page ring must cover HBM
+// latency x the CTA's share of the bandwidth plus the consumers' per-item epilogue: 8 stages.
+// A depth that is not a multiple of the 4 consumer warps needs stage sequence numbers: pages go
+// to warps round-robin inside an item, so the previous use of a stage may belong to another,
+// lagging warp and still be in flight, and a parity-only wait would return on the older phase;
+// with `seq` the consumer of page q first waits until the producer armed the stage for q.  With
+// 8 stages page q - 8 was consumed by the same warp (or before the item barrier), so the check is
+// compiled out.  (Measured: 10 stages + seq for G <= 4 changed C2/C3/C4 by -1..+1% and small
+// batches by +2%; not kept.)
+#ifndef L4_STAGES_SMALL_G
+#define L4_STAGES_SMALL_G 8
+#endif
 template <int G>
 struct SmemLayout {
-  static constexpr int stages_n = 8;
-  static_assert(stages_n % kConsumerWarps == 0, "stage parity waits need stages % consumer warps == 0");
+  static constexpr int stages_n = G == 8 ? 8 : L4_STAGES_SMALL_G;
   static constexpr int qslot_bytes = G * kHeadDim * 2;
   static constexpr int merge_bytes =
       align16c(cmax(kConsumerWarps * G * kMergeStride * 4, cmax(kPlanScratchBytes, kCombineScratchBytes)));
@@ -547,7 +555,8 @@ struct SmemLayout {
   static constexpr int merge_l = merge_m + kConsumerWarps * kMaxG * 4;
   static constexpr int bars = merge_l + kConsumerWarps * kMaxG * 4;
   static constexpr int nbars = 2 * stages_n + 2 * kItemSlots;
-  static constexpr int flag = bars + nbars * 8;
+  static constexpr int seq = bars + nbars * 8;  // int [stages_n]: page sequence number armed per stage
+  static constexpr int flag = seq + stages_n * 4;
   static constexpr int total = align16c(flag + 16);
   static constexpr int alloc = total + 1024;  // room to align the base to 1024 B (128B swizzle)
   static_assert(merge_o % 16 == 0 && total % 16 == 0 && bars % 8 == 0, "aligned areas");
@@ -806,7 +815,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) L4_MARK(0);
+  volatile int* s_seq = reinterpret_cast<volatile int*>(smem + SL::seq);
   if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) s_seq[i] = -1;
     for (int i = 0; i < kStages; ++i) {
       mbar_init(bar_full + i * 8, 1);
       mbar_init(bar_empty + i * 8, 1);
@@ -866,6 +877,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == kConsumerWarps) {
     // ============================== producer warp: items, Q and KV pages via TMA
+#ifdef L4_TRACE
+    L4_TRACE_ACC
+#endif
     const uint64_t policy = policy_evict_first();
     bool exhausted = false;
     // Dynamic LPT scheduling: the first item is blockIdx.x, later ones come from an atomic
@@ -912,6 +926,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #endif
       const uint32_t fb = bar_full + st * 8;
       mbar_arrive_expect_tx(fb, kStageBytes);
+      if constexpr (kStages % kConsumerWarps != 0)
+        st_release_cta(sbase + SL::seq + st * 4, (int)qseq);  // stage armed for page qseq
       const int row = (page * a.Hkv + h) * kPage;
       const uint32_t dst = sbase + SL::stages + st * kStageBytes;
       tma_load_3d(dst, &tmK, 0, row, 0, fb, policy);
@@ -995,6 +1011,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         a.header->sched_done = 0;
       }
     }
+#ifdef L4_TRACE
+    if (lane == 0) L4_TRACE_FLUSH(14);
+#endif
     // sentinel: tell the consumers there is no more work
     if (lane == 0) {
       const uint32_t slot = k % kItemSlots;
@@ -1006,6 +1025,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 
   // ============================== consumer warps
+#ifdef L4_TRACE
+  L4_TRACE_ACC
+#endif
   const int g = lane >> 2, c = lane & 3;
   const int ct = threadIdx.x;  // 0..127
   // split bookkeeping for the deferred two-level combine (see the epilogue below)
@@ -1018,9 +1040,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     return a.counters + (size_t)w.b * a.Hkv + w.h;
   };
   auto finish_group = [&](const WorkItem& w) {  // this CTA was the last split of w's group
-#ifdef L4_TRACE
-    if (ct == 0) L4_MARK(10);
-#endif
     const int ns = w.nsplit;
     const int ng = (ns + kCombineGroup - 1) / kCombineGroup;
     const int g0 = (w.split / kCombineGroup) * kCombineGroup;
@@ -1038,9 +1057,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       named_bar_sync(1, kConsumerThreads);
       if (*s_flag) combine_slots<G>(a, merge_o, w.part_base, kCombineGroup, ng, true, row0, 0, ct);
     }
-#ifdef L4_TRACE
-    if (ct == 0) L4_MARK(11);
-#endif
   };
   bool has_pend = false;
   WorkItem pend_it;
@@ -1049,7 +1065,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint32_t qbase = 0;
   for (uint32_t k = 0;; ++k) {
     const uint32_t slot = k % kItemSlots;
+#ifdef L4_TRACE
+    const unsigned long long ti0 = trace_now();
+#endif
     mbar_wait(bar_ifull + slot * 8, (k / kItemSlots) & 1);
+#ifdef L4_TRACE
+    if (ct == 0) trace_add(10, trace_now() - ti0);
+#endif
     const WorkItem it = s_items[slot].it;
     const int item_idx = s_items[slot].idx;
     if (it.b < 0) break;
@@ -1081,13 +1103,23 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef L4_TRACE
       const unsigned long long tw0 = trace_now();
 #endif
+      if constexpr (kStages % kConsumerWarps != 0) {
+        while (ld_acquire_cta(sbase + SL::seq + st * 4) != (int)q) {
+        }
+      }
       mbar_wait(bar_full + st * 8, (q / kStages) & 1);
 #ifdef L4_TRACE
       if (q == 0 && lane == 0) L4_MARK(4);
       if (warp == 0 && lane == 0) trace_add(12, trace_now() - tw0);
 #endif
       const int valid = (j == np - 1) ? it.last_valid : kPage;
+#ifdef L4_TRACE
+      const unsigned long long tc0 = trace_now();
+#endif
       consume_page(sbase + SL::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane);
+#ifdef L4_TRACE
+      if (warp == 0 && lane == 0) trace_add(11, trace_now() - tc0);
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + st * 8);
     }
@@ -1197,7 +1229,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     named_bar_sync(1, kConsumerThreads);
     if (*s_flag) finish_group(pend_it);
   }
-  if (threadIdx.x == 0) L4_MARK(5);
+  if (threadIdx.x == 0) {
+    L4_MARK(5);
+#ifdef L4_TRACE
+    L4_TRACE_FLUSH(10);
+    L4_TRACE_FLUSH(11);
+    L4_TRACE_FLUSH(12);
+    L4_TRACE_FLUSH(13);
+    L4_TRACE_FLUSH(15);
+#endif
+  }
 }
 
 // =================================================================== host side

@@ -57,19 +57,20 @@ def main():
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (4096 * 16))()
     l4.lib().l4_trace_read(buf, 4096 * 16)
-    t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, :12].astype(np.float64)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, :10].astype(np.float64)
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
     bytes_kv = wl.bytes_kv
     print(f"{args.workload} {args.bin} {args.mode}: {bytes_kv / 1e6:.0f} MB KV, event {a.elapsed_time(b) * 1e3:.1f} us, {ncta} CTAs")
     acc = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, 12:16].astype(np.float64)
+    acc2 = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16)[:ncta, 10:12].astype(np.float64)
     span = (t[:, 5] - t[:, 0]) / 1e3
     print(f"  per CTA (us, median over CTAs): busy {np.median(span):.1f}; consumer warp0 waiting for data "
           f"{np.median(acc[:, 0]) / 1e3:.1f}; item epilogues {np.median(acc[:, 1]) / 1e3:.1f}; producer waiting "
           f"for ring slots {np.median(acc[:, 2]) / 1e3:.1f}; items {np.median(acc[:, 3]):.0f} "
-          f"(min {acc[:, 3].min():.0f}, max {acc[:, 3].max():.0f})")
-    for k, name in enumerate(["entry", "pdl_wait", "plan", "tma0", "land0", "done", "p_load", "p_count", "p_pass1", "p_pass2",
-                                   "comb_beg", "comb_end"]):
+          f"(min {acc[:, 3].min():.0f}, max {acc[:, 3].max():.0f}); consumer warp0 waiting for the next item "
+          f"(Q) {np.median(acc2[:, 0]) / 1e3:.1f}; warp0 page compute {np.median(acc2[:, 1]) / 1e3:.1f}")
+    for k, name in enumerate(["entry", "pdl_wait", "plan", "tma0", "land0", "done", "p_load", "p_count", "p_pass1", "p_pass2"]):
         c = rel[:, k]
         c = c[(c > -1e6) & (c < 1e7)]  # marks a CTA never reached hold stale values
         if c.size == 0:
