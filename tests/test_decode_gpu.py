@@ -181,7 +181,8 @@ def test_empty_batch_and_all_empty_requests():
 
 
 def _sampled_full_size(lens, shape, seed, samples):
-    """Full-size parity in the bench launch configuration (auto plan), on sampled requests."""
+    """Full-size parity in the bench launch configuration (auto plan, single launch, early inputs,
+    back to back), on sampled requests; the early-input calls are bit-identical to a plain call."""
     table = synth.make_page_table(lens, seed=seed, spare_pages=64)
     g = torch.Generator(device="cuda").manual_seed(seed)
     B = table.batch
@@ -192,7 +193,14 @@ def _sampled_full_size(lens, shape, seed, samples):
     ix = torch.from_numpy(table.indices).cuda()
     kl = torch.from_numpy(table.kv_len).cuda()
     out, lse = l4.decode_attention(q, k, v, ip, ix, kl)
+    # bench.py's launch configuration: back-to-back single-launch calls with early inputs
+    params = l4.make_params(B, shape.num_q_heads, shape.num_kv_heads, flags=l4.L4_DECODE_EARLY_INPUTS)
+    ws = l4.alloc_workspace(params, table.total_pages)
+    o2, l2 = torch.empty_like(out), torch.empty_like(lse)
+    for _ in range(3):
+        l4.attention_call(params, q, k, v, ip, ix, kl, table.total_pages, o2, l2, ws)
     torch.cuda.synchronize()
+    assert torch.equal(o2, out) and torch.equal(l2, lse)
     ro, rl = oa.paged_decode_attention(q, k, v, table.indptr, table.indices, table.kv_len, shape.num_kv_heads,
                                        requests=samples)
     o = out.double().cpu().numpy()
