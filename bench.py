@@ -452,6 +452,38 @@ def migration_bandwidth(reps: int = 10):
                 note="loopback src->dst on one GPU; HBM traffic = read + write; 4096 32 KB slices")
 
 
+def partition_speed():
+    """l4_partition (host C++) over 10,000 ShareGPT-like requests (lengths up
+    to 128K) at E = 4, 8, 16 instances; the paper plans E = 16 in 0.06 s."""
+    from paper_2512_19179_b200 import l4
+    I, O = synth.requests_sharegpt_like(seed=1, n=10000)
+    D = synth.roofline_qoe_d()
+    res = {}
+    for E in (4, 8, 16):
+        t = time.perf_counter()
+        stages, obj = l4.partition(I, O, E, D, 7e11, 131072, mode=0)
+        dt = time.perf_counter() - t
+        t = time.perf_counter()
+        l4.partition(I, O, E, D, 7e11, 131072, mode=0, algorithm=l4.PART_TWO_PHASE)
+        dt2 = time.perf_counter() - t
+        res[f"E{E}"] = dict(exact_dp_ms=round(dt * 1e3, 3), two_phase_ms=round(dt2 * 1e3, 3), stages=stages,
+                            objective=obj)
+    return res
+
+
+def partition_oracle_speed():
+    """The partition oracle (pure Python, one core) on the same M6 inputs (cpu_baseline leg)."""
+    from oracle import partition as op
+    I, O = synth.requests_sharegpt_like(seed=1, n=10000)
+    D = synth.roofline_qoe_d()
+    res = {}
+    for E in (4, 16):
+        t = time.perf_counter()
+        op.plan_dp(I, O, E, D, 7e11, 131072, mode=0)
+        res[f"E{E}_s"] = round(time.perf_counter() - t, 3)
+    return res
+
+
 # ----------------------------------------------------------------------------- pipeline (N > 1)
 def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, seed=0, shape=None, precopy_lead=0,
                      policy="least_loaded", rebalance_every=0):
@@ -719,6 +751,7 @@ def main():
         extra = mixed_vs_binned(max(5, args.steps // 2), 3)
         extra["fig2_heterogeneity"] = heterogeneity_slowdown(max(5, args.steps // 2), 3)
         extra["migration"] = migration_bandwidth()
+        extra["partition_m6"] = partition_speed()
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(args.workload, budget_s=12.0)
@@ -777,6 +810,8 @@ def main():
     }
     if cpu:
         line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if not args.no_extra:
+            line["cpu_baseline"]["partition_m6_oracle"] = partition_oracle_speed()
     if extra:
         line["extra"] = extra
     print(json.dumps(line), flush=True)
