@@ -135,11 +135,11 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workload
 class Workload:
-    def __init__(self, name: str, lens, shape, seed: int = 0, device="cuda"):
+    def __init__(self, name: str, lens, shape, seed: int = 0, device="cuda", layout: str = "fragmented"):
         import torch
         self.name, self.shape = name, shape
         self.lens = np.asarray(lens, dtype=np.int64)
-        self.table = synth.make_page_table(self.lens, seed=seed, spare_pages=64)
+        self.table = synth.make_page_table(self.lens, seed=seed, spare_pages=64, layout=layout)
         g = torch.Generator(device=device).manual_seed(seed)
         B, t = len(self.lens), self.table
         self.q = torch.randn(B, shape.num_q_heads, 128, device=device, generator=g).to(torch.bfloat16)
@@ -370,6 +370,18 @@ def mixed_vs_binned(steps: int, warmup: int):
                      items=info.num_items, chunk_pages=info.chunk_pages)
     del w
     torch.cuda.empty_cache()
+    # SURVEY §8(d) variants: C3 "production-like" (16 long, short median 2048), C2 with a partial
+    # last page (L = 1000, the paper's "1000-token"), C2 with an identity page layout
+    variants = (("c3_production", synth.lengths_c3_production(0), shape, "fragmented"),
+                ("c2_L1000", synth.lengths_c2(length=1000), shape, "fragmented"),
+                ("c2_contiguous", synth.lengths_c2(), shape, "contiguous"))
+    for name, lens_v, shape_v, layout in variants:
+        w = Workload(name, lens_v, shape_v, layout=layout)
+        t, _, _ = time_steps(w, steps, warmup)
+        res[name] = dict(gbs=round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1), ms=round(t / steps, 4),
+                         sum_len=int(np.sum(lens_v)), layout=layout)
+        del w
+        torch.cuda.empty_cache()
     return res
 
 

@@ -79,6 +79,19 @@ def lengths_c3(seed: int = 0, n_short: int = 248, n_long: int = 8) -> np.ndarray
     return np.concatenate([short, long])
 
 
+def lengths_c3_production(seed: int = 0, n_short: int = 240, n_long: int = 16) -> np.ndarray:
+    """SURVEY §8(d) M3 "production-like" variant of C3: batch 256, 16 long requests and a short
+    median of 2048 (seed 0: sum L = 1,870,679)."""
+    rng = np.random.default_rng(seed)
+    short = np.clip(np.round(np.exp(rng.normal(math.log(2048.0), 1.0, n_short))), 100, 16383)
+    long = np.round(np.exp(rng.uniform(math.log(16384.0), math.log(131072.0), n_long)))
+    short = short.astype(np.int64)
+    long = long.astype(np.int64)
+    short[0] = 100
+    long[-1] = 131072
+    return np.concatenate([short, long])
+
+
 def lengths_c4(seed: int = 0, batch: int = 32) -> np.ndarray:
     """BASELINE.json configs[3]: long-context batch 32 with lengths 32K..128K."""
     rng = np.random.default_rng(seed)
