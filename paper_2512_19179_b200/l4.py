@@ -203,6 +203,12 @@ def alloc_workspace(params: DecodeParams, max_total_pages: int, device=None):
                        device=device if device is not None else "cuda")
 
 
+def workspace_init(params: DecodeParams, workspace, stream=None) -> None:
+    """l4_decode_workspace_init: zero the scheduler header and split counters of a workspace."""
+    _check(lib().l4_decode_workspace_init(ctypes.byref(params), _ptr(workspace), workspace.numel(),
+                                          _stream_handle(stream)))
+
+
 def decode_plan(params: DecodeParams, kv_len, page_indptr, total_pages: int, workspace, stream=None):
     import torch
     _need(kv_len, torch.int32, "kv_len")

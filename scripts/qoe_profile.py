@@ -5,7 +5,7 @@ latency of each request in the batch = the step time (every request in th
 stretched to the same iteration time).  Decode-only profile: F = (1, n, sum I, sum I^2, sum L)
 with the mask {1, n, sum L} (reading Z38).  Validation on held-out mixed batches drawn from the
 ShareGPT-like generator (Fig. 13 `fig:prediction`: 8.9% vs 64% for a static
-predictor).  Writes profiles/qoe_fit_<tag>.json.
+predictor).  Writes gpurun_out/qoe_fit_<tag>.json (committed copies live in profiles/).
 """
 import argparse
 import json
@@ -54,8 +54,7 @@ def step_time(pool, lens, shape, rng, reps=7):
     for r in range(reps + 2):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        l4.decode_plan(p, kl, ip, int(ptr[-1]), ws)
-        l4.decode_run(p, pool.q[:B], pool.k, pool.v, ix, pool.out[:B], pool.lse[:B], ws)
+        l4.attention_call(p, pool.q[:B], pool.k, pool.v, ip, ix, kl, int(ptr[-1]), pool.out[:B], pool.lse[:B], ws)
         b.record()
         b.synchronize()
         if r >= 2:
@@ -106,7 +105,7 @@ def main():
     rel = (pred - Qv) / Qv
     static = (np.mean(Q) - Qv) / Qv
     res = dict(
-        method="P:319-323 profiling grid on B200 (decode step = l4_decode_plan + l4_decode_run, one layer, "
+        method="P:319-323 profiling grid on B200 (decode step = one single-launch l4_decode_attention, one layer, "
                "Llama-3-8B attention shape); OLS by l4_qoe_fit with mask {1, n, sum L} (Z38)",
         D=D.tolist(), rms_seconds=rms, n_fit=int(len(Q)), n_validation=int(len(Qv)),
         mean_abs_rel_error=float(np.mean(np.abs(rel))), p95_abs_rel_error=float(np.percentile(np.abs(rel), 95)),
@@ -115,8 +114,9 @@ def main():
         implied_bandwidth_GBps=float(4 * shape.num_kv_heads * 128 / D[4] / 1e9) if D[4] > 0 else None,
         grid=grid, validation=[dict(batch=int(f[1]), sum_len=int(f[4]), seconds=float(q), predicted=float(p))
                                for f, q, p in zip(Fv, Qv, pred)])
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    path = os.path.join(ROOT, "profiles", f"qoe_fit_{args.tag}.json")
+    # written under gpurun_out/ (what gpurun brings back); copy to profiles/ to commit it
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    path = os.path.join(ROOT, "gpurun_out", f"qoe_fit_{args.tag}.json")
     json.dump(res, open(path, "w"), indent=1)
     print(json.dumps({k: v for k, v in res.items() if k not in ("grid", "validation")}))
 

@@ -331,3 +331,32 @@ def test_two_level_combine_group_boundaries(G):
     ob, lb = _run_gpu(table, q, k, v, chunk_pages=1, out_dtype=l4.L4_DT_BF16)
     assert np.max(np.abs(ob - ro) - np.abs(ro) * 2.0 ** -8) <= TOL
     _check(ob * 0, lb, ro * 0, rl)
+
+
+def test_workspace_init_and_block_table_layout():
+    """A dirty workspace is made usable by l4_decode_workspace_init; a fixed-stride block table
+    (indptr[b] = slot_b * max_pages, gaps between requests) is a valid page table (l4.h)."""
+    lens = np.array([5, 300, 0, 2048, 17, 999], dtype=np.int64)
+    shape, table, q, k, v, ro, rl = _case(lens, 16, 4, seed=31)
+    max_pages = 200
+    slots = np.array([3, 0, 5, 1, 4, 2])
+    bt = np.full(6 * max_pages, -1, dtype=np.int32)
+    indptr = np.zeros(7, dtype=np.int32)
+    for b in range(6):
+        n = table.indptr[b + 1] - table.indptr[b]
+        bt[slots[b] * max_pages: slots[b] * max_pages + n] = table.indices[table.indptr[b]:table.indptr[b + 1]]
+        indptr[b] = slots[b] * max_pages
+    indptr[6] = 6 * max_pages  # not read
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    ip, ix, kl = torch.from_numpy(indptr).cuda(), torch.from_numpy(bt).cuda(), torch.from_numpy(table.kv_len).cuda()
+    for flags in (0, l4.L4_DECODE_EARLY_INPUTS):
+        params = l4.make_params(6, 16, 4, chunk_pages=3, flags=flags)
+        ws = l4.alloc_workspace(params, bt.size)
+        ws.fill_(0xFF)  # stale scheduler state and counters
+        l4.workspace_init(params, ws)
+        out = torch.empty(6, 16, 128, device="cuda")
+        lse = torch.empty(6, 16, device="cuda")
+        for _ in range(2):
+            l4.attention_call(params, qd, kd, vd, ip, ix, kl, bt.size, out, lse, ws)
+        torch.cuda.synchronize()
+        _check(out.double().cpu().numpy(), lse.double().cpu().numpy(), ro, rl)
