@@ -1540,7 +1540,10 @@ extern "C" l4_status l4_decode_attention(const l4_decode_params* p, const void* 
                                          void* stream) {
   // One launch: every CTA of the decode kernel plans in its own shared memory (B <= 1024).
   // Larger batches: the materialised plan (planner kernel) followed by the run.
-  if (p && p->batch > 0 && p->batch <= kFusedMaxBatch) {
+  int G = 0;
+  const l4_status ps = check_params(p, &G);  // parameter errors first, as in plan / run
+  if (ps != L4_OK) return ps;
+  if (p->batch > 0 && p->batch <= kFusedMaxBatch) {
     L4_CHECK_ARG(kv_len != nullptr, "kv_len is NULL");
     return run_impl(p, q, k_pages, v_pages, num_pages, page_indices, out, lse, workspace, workspace_bytes,
                     static_cast<cudaStream_t>(stream), kv_len, page_indptr, total_pages);

@@ -170,12 +170,22 @@ def test_decode_param_validation():
     for kw, status in [(dict(head_dim=64), l4.L4_ERR_UNSUPPORTED), (dict(page_size=32), l4.L4_ERR_UNSUPPORTED),
                        (dict(num_q_heads=12, num_kv_heads=8), l4.L4_ERR_INVALID_ARG),
                        (dict(num_q_heads=48, num_kv_heads=3), l4.L4_ERR_UNSUPPORTED),
-                       (dict(batch=-1), l4.L4_ERR_INVALID_ARG)]:
+                       (dict(batch=-1), l4.L4_ERR_INVALID_ARG),
+                       (dict(batch=8193), l4.L4_ERR_UNSUPPORTED),
+                       (dict(flags=2), l4.L4_ERR_INVALID_ARG),
+                       (dict(out_dtype=7), l4.L4_ERR_INVALID_ARG),
+                       (dict(sm_scale=float("nan")), l4.L4_ERR_INVALID_ARG)]:
         args = dict(batch=4, num_q_heads=8, num_kv_heads=2, head_dim=128, page_size=16)
         args.update(kw)
         p = l4.make_params(**args)
-        st = L.l4_decode_plan(p, None, None, 0, None, 0, None)
-        assert st == status, (kw, st, L.l4_last_error())
+        for st in (L.l4_decode_plan(p, None, None, 0, None, 0, None),
+                   L.l4_decode_attention(p, None, None, None, 1, None, None, 0, None, None, None, None, 0, None),
+                   L.l4_decode_workspace_init(p, None, 0, None)):
+            assert st == status, (kw, st, L.l4_last_error())
+    # valid parameters, missing buffers: argument / workspace errors before any device work
+    p = l4.make_params(4, 8, 2)
+    assert L.l4_decode_workspace_init(p, None, 0, None) == l4.L4_ERR_WORKSPACE
+    assert L.l4_decode_plan_info(None, None, None) == l4.L4_ERR_INVALID_ARG
 
 
 def test_two_phase_bit_exact_with_oracle():
