@@ -159,6 +159,17 @@ l4_status l4_decode_plan_info(const void* workspace, l4_plan_info* info_out, voi
  * Test/diagnostic use only. */
 l4_status l4_decode_plan_items(const void* workspace, int32_t* items_out, int32_t max_items, void* stream);
 
+/* Debug check of a page table before decode (the hot path trusts it): on the device, for every
+ * request b: kv_len[b] >= 0; indptr[b] >= 0 and indptr[b] + ceil(kv_len[b]/16) <= total_pages;
+ * every page id the request reads lies in [0, num_pages); and no page id is read by two
+ * requests or twice by one (a page belongs to one sequence).  Writes to host `report`:
+ * [0] number of violations, [1] first offending request (or -1), [2] its violation kind
+ * (1 length, 2 indptr range, 3 page id range, 4 page shared).  Synchronises `stream`.  The
+ * uniqueness check uses `scratch` (device, >= num_pages int32, overwritten). */
+l4_status l4_decode_validate(const l4_decode_params* p, const int32_t* kv_len, const int32_t* page_indptr,
+                             const int32_t* page_indices, int64_t total_pages, int64_t num_pages,
+                             int32_t* scratch, int32_t* report, void* stream);
+
 /* ========================================================================
  * 2. Length-aware stage partition (§4.2) — host code
  *

@@ -1572,6 +1572,87 @@ extern "C" l4_status l4_decode_plan_info(const void* workspace, l4_plan_info* in
   return L4_OK;
 }
 
+namespace l4 {
+namespace {
+// l4_decode_validate: one warp per request; report[0] counts violations, report[1..2] keep the
+// lowest offending request and its kind (atomicMin on (request << 3 | kind)).
+__global__ void validate_kernel(const int* kv_len, const int* indptr, const int* indices, int B, long long total_pages,
+                                long long num_pages, int* owner, int* report) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  const int b = warp;
+  const int L = kv_len[b];
+  int kind = 0;
+  long long np = 0, base = indptr[b];
+  if (L < 0) {
+    kind = 1;
+  } else {
+    np = (L + kPage - 1) / kPage;
+    if (base < 0 || base + np > total_pages) kind = 2;
+  }
+  if (kind == 0) {
+    for (long long j = lane; j < np; j += 32) {
+      const int pg = indices[base + j];
+      int k2 = 0;
+      if (pg < 0 || pg >= num_pages) {
+        k2 = 3;
+      } else if (atomicCAS(owner + pg, -1, b) != -1) {
+        k2 = 4;  // already claimed (by another request, or twice by this one)
+      }
+      const unsigned bad = __ballot_sync(__activemask(), k2 != 0);
+      if (bad && kind == 0) kind = __shfl_sync(__activemask(), k2, __ffs(bad) - 1);
+    }
+    kind = __reduce_max_sync(0xffffffffu, kind);
+  }
+  if (lane == 0 && kind != 0) {
+    atomicAdd(report, 1);
+    atomicMin(report + 1, (b << 3) | kind);
+  }
+}
+}  // namespace
+}  // namespace l4
+
+extern "C" l4_status l4_decode_validate(const l4_decode_params* p, const int32_t* kv_len, const int32_t* page_indptr,
+                                        const int32_t* page_indices, int64_t total_pages, int64_t num_pages,
+                                        int32_t* scratch, int32_t* report, void* stream) {
+  int G = 0;
+  l4_status s = check_params(p, &G);
+  if (s != L4_OK) return s;
+  L4_CHECK_ARG(report != nullptr, "report is NULL");
+  L4_CHECK_ARG(total_pages >= 0 && num_pages >= 1, "total_pages < 0 or num_pages < 1");
+  report[0] = 0;
+  report[1] = -1;
+  report[2] = 0;
+  if (p->batch == 0) return L4_OK;
+  L4_CHECK_ARG(kv_len && page_indptr && scratch, "kv_len / page_indptr / scratch is NULL");
+  L4_CHECK_ARG(total_pages == 0 || page_indices, "page_indices is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* d_report = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_report), 2 * sizeof(int), st);
+  const int init[2] = {0, INT_MAX};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_report, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0xff, (size_t)num_pages * sizeof(int), st);
+  if (e == cudaSuccess) {
+    const int threads = 256, blocks = (int)((p->batch * 32LL + threads - 1) / threads);
+    validate_kernel<<<blocks, threads, 0, st>>>(kv_len, page_indptr, page_indices, p->batch, total_pages, num_pages,
+                                                scratch, d_report);
+    e = cudaGetLastError();
+  }
+  int h[2] = {0, INT_MAX};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_report, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (d_report) cudaFreeAsync(d_report, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    set_error("l4_decode_validate: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return L4_ERR_CUDA;
+  }
+  report[0] = h[0];
+  report[1] = h[0] ? (h[1] >> 3) : -1;
+  report[2] = h[0] ? (h[1] & 7) : 0;
+  return L4_OK;
+}
+
 extern "C" l4_status l4_decode_plan_items(const void* workspace, int32_t* items_out, int32_t max_items, void* stream) {
   L4_CHECK_ARG(workspace && items_out && max_items >= 0, "bad arguments");
   PlanHeader h;

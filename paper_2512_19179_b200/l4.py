@@ -23,7 +23,7 @@ _STATUS_NAMES = ["OK", "INVALID_ARG", "UNSUPPORTED", "CUDA", "WORKSPACE", "NO_PA
 
 EXPORTED_SYMBOLS = (
     "l4_last_error", "l4_version", "l4_decode_workspace_size", "l4_decode_workspace_init", "l4_decode_plan", "l4_decode_run",
-    "l4_decode_attention", "l4_decode_plan_info", "l4_decode_plan_items", "l4_partition", "l4_pool_create",
+    "l4_decode_attention", "l4_decode_plan_info", "l4_decode_plan_items", "l4_decode_validate", "l4_partition", "l4_pool_create",
     "l4_pool_alloc", "l4_pool_free", "l4_pool_num_free", "l4_pool_destroy", "l4_migrate", "l4_copy_pages",
     "l4_pack_pages", "l4_unpack_pages", "l4_ipc_get_handle", "l4_ipc_open_handle", "l4_ipc_close_handle",
     "l4_enable_peer_access", "l4_refine_boundary", "l4_qoe_fit",
@@ -103,6 +103,8 @@ def lib() -> ctypes.CDLL:
     L.l4_decode_attention.argtypes = [P(DecodeParams), vp, vp, vp, i64, vp, vp, i64, vp, vp, vp, vp, sz, vp]
     L.l4_decode_plan_info.restype = ctypes.c_int
     L.l4_decode_plan_info.argtypes = [vp, P(PlanInfo), vp]
+    L.l4_decode_validate.restype = ctypes.c_int
+    L.l4_decode_validate.argtypes = [P(DecodeParams), vp, vp, vp, i64, i64, vp, vp, vp]
     L.l4_decode_plan_items.restype = ctypes.c_int
     L.l4_decode_plan_items.argtypes = [vp, vp, i32, vp]
     L.l4_partition.restype = ctypes.c_int
@@ -269,6 +271,21 @@ def attention_call(params: DecodeParams, q, k_pages, v_pages, page_indptr, page_
                                      int(k_pages.shape[0]), _ptr(page_indptr), _ptr(page_indices), int(total_pages),
                                      _ptr(kv_len), _ptr(out), _ptr(lse), _ptr(workspace), workspace.numel(),
                                      _stream_handle(stream)))
+
+
+def validate(params: DecodeParams, kv_len, page_indptr, page_indices, num_pages: int, stream=None):
+    """l4_decode_validate (debug): returns (violations, first offending request, kind) with kind
+    1 length < 0, 2 indptr range, 3 page id range, 4 page read by two requests / twice."""
+    import torch
+    _need(kv_len, torch.int32, "kv_len")
+    _need(page_indptr, torch.int32, "page_indptr")
+    _need(page_indices, torch.int32, "page_indices")
+    scratch = torch.empty(max(int(num_pages), 1), dtype=torch.int32, device=kv_len.device)
+    rep = (ctypes.c_int32 * 3)()
+    _check(lib().l4_decode_validate(ctypes.byref(params), _ptr(kv_len), _ptr(page_indptr), _ptr(page_indices),
+                                    int(page_indices.numel()), int(num_pages), _ptr(scratch), rep,
+                                    _stream_handle(stream)))
+    return int(rep[0]), int(rep[1]), int(rep[2])
 
 
 def plan_info(workspace, stream=None) -> PlanInfo:

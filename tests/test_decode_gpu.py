@@ -360,3 +360,25 @@ def test_workspace_init_and_block_table_layout():
             l4.attention_call(params, qd, kd, vd, ip, ix, kl, bt.size, out, lse, ws)
         torch.cuda.synchronize()
         _check(out.double().cpu().numpy(), lse.double().cpu().numpy(), ro, rl)
+
+
+def test_validate_page_table():
+    """l4_decode_validate flags each kind of page-table corruption and passes a valid table."""
+    lens = np.array([5, 300, 0, 2048, 17], dtype=np.int64)
+    table = synth.make_page_table(lens, seed=3, spare_pages=10)
+    params = l4.make_params(5, 8, 2)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    assert l4.validate(params, dev(table.kv_len), dev(table.indptr), dev(table.indices), table.num_pages) == (0, -1, 0)
+    kl = table.kv_len.copy()
+    kl[3] = -1
+    assert l4.validate(params, dev(kl), dev(table.indptr), dev(table.indices), table.num_pages) == (1, 3, 1)
+    kl = table.kv_len.copy()
+    kl[4] = 5000  # runs past the end of the page table
+    assert l4.validate(params, dev(kl), dev(table.indptr), dev(table.indices), table.num_pages) == (1, 4, 2)
+    ix = table.indices.copy()
+    ix[table.indptr[1] + 7] = table.num_pages  # out of the pool
+    assert l4.validate(params, dev(table.kv_len), dev(table.indptr), dev(ix), table.num_pages) == (1, 1, 3)
+    ix = table.indices.copy()
+    ix[table.indptr[3] + 2] = ix[table.indptr[1]]  # request 3 reads request 1's page
+    n, first, kind = l4.validate(params, dev(table.kv_len), dev(table.indptr), dev(ix), table.num_pages)
+    assert n == 1 and first in (1, 3) and kind == 4
