@@ -464,6 +464,18 @@ def migration_bandwidth(reps: int = 10):
                 note="loopback src->dst on one GPU; HBM traffic = read + write; 4096 32 KB slices")
 
 
+def fitted_qoe_d(layers: int = 32):
+    """Eq. (1)'s D fitted on this kernel's measured step times (NEXT#3, the newest committed
+    profiles/qoe_fit_*.json, one layer) scaled to a `layers`-layer decode step; else None (the
+    partition then uses the roofline D, Z15)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "qoe_fit_r*.json")))
+    if not files:
+        return None, "roofline (synth.roofline_qoe_d, Z15)"
+    d = json.load(open(files[-1]))["D"]
+    return tuple(float(x) * layers for x in d), f"fitted ({os.path.relpath(files[-1], ROOT)}) x {layers} layers"
+
+
 def partition_speed():
     """l4_partition (host C++) over 10,000 ShareGPT-like requests (lengths up
     to 128K) at E = 4, 8, 16 instances; the paper plans E = 16 in 0.06 s."""
@@ -578,7 +590,8 @@ def pipeline_line(args, world, rank, local):
     device = torch.device("cuda", local)
     cdev = device if dist.get_backend() == "nccl" else torch.device("cpu")   # collectives' device
     peak, peak_src = load_peaks()
-    stages, obj = pipeline.plan_stages(world, seed=0)
+    qoe_d, qoe_src = fitted_qoe_d()
+    stages, obj = pipeline.plan_stages(world, seed=0, qoe_d=qoe_d)
     rr = [(0, stages[-1][1], world)]                       # length-agnostic: one stage of all instances
     res = {}
     dist.barrier()                                          # first collective on the group
@@ -631,7 +644,8 @@ def pipeline_line(args, world, rank, local):
         "config": {"workload": "c5-pipeline", "desc": "BASELINE configs[4]: length-aware pipeline, "
                    f"{world} instances (1 GPU each), Llama-3-8B attention shape, ShareGPT-like closed loop, "
                    f"{256} resident requests per instance, 1.2M-token KV budget per instance",
-                   "stages": l4r["stages"], "partition_objective": obj,
+                   "stages": l4r["stages"], "partition_objective": obj, "qoe_d": list(qoe_d) if qoe_d else None,
+                   "qoe_d_source": qoe_src,
                    "parallelism": f"length-aware pipeline over {world} GPUs (l4_partition); KV migration over NCCL P2P",
                    "l2": "inputs larger than L2; no flush"},
         "tokens_per_s": round(l4r["tokens_per_s"], 1),
