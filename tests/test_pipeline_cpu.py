@@ -1,4 +1,4 @@
-"""Multi-process CPU tests (gloo, world_size 2 and 3) of the length-aware pipeline's host logic:
+"""Multi-process CPU tests (gloo, world_size 2, 3 and 4) of the length-aware pipeline's host logic:
 the replicated control plane agrees on every rank, the migration transport moves exactly the
 migrating request's pages, page accounting is conserved, and the P2P exchange never deadlocks.
 Device kernels are replaced by CPU mocks HERE (test-only); the product path uses libl4."""
@@ -86,13 +86,13 @@ class MockOps:
         return nbytes
 
 
-def _worker(rank, world, port, stages, steps, out_q, lead=0):
+def _worker(rank, world, port, stages, steps, out_q, lead=0, policy="least_loaded", rebalance_every=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         sim = pipeline.ClusterSim(stages, concurrency=48 * world, seed=5, token_budget=400_000, batch_cap=256,
-                                  precopy_lead=lead)
+                                  precopy_lead=lead, policy=policy, rebalance_every=rebalance_every)
         ops = MockOps()
         rt = pipeline.RankRuntime(sim, rank, num_pages=400_000 // 16 * 2, shape=None, ops=ops)
         pool = rt.pool
@@ -138,13 +138,22 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,lead", [(2, 0), (3, 0), (2, 6), (3, 3)])
-def test_pipeline_gloo_migrations(world, lead):
-    stages = [(0, 1500, 1), (1500, 262144, world - 1)]
+@pytest.mark.parametrize("world,lead,policy", [(2, 0, "least_loaded"), (3, 0, "least_loaded"), (2, 6, "least_loaded"),
+                                               (3, 3, "least_loaded"), (4, 4, "bidask")])
+def test_pipeline_gloo_migrations(world, lead, policy):
+    """world 4 (bid-ask receivers, rebalancing checks every 10 steps, live migration): three
+    stages, the middle one with two instances, so handovers go between four rank pairs
+    (0->1, 0->2, 1->3, 2->3); the transport is the same for rebalancing moves."""
+    if world == 4:
+        stages = [(0, 1000, 1), (1000, 3000, 2), (3000, 262144, 1)]
+    else:
+        stages = [(0, 1500, 1), (1500, 262144, world - 1)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, stages, 120, q, lead)) for r in range(world)]
+    reb = 10 if policy == "bidask" else 0
+    procs = [ctx.Process(target=_worker, args=(r, world, port, stages, 120, q, lead, policy, reb))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
