@@ -165,7 +165,8 @@ l4_status l4_decode_plan_items(const void* workspace, int32_t* items_out, int32_
  * requests or twice by one (a page belongs to one sequence).  Writes to host `report`:
  * [0] number of violations, [1] first offending request (or -1), [2] its violation kind
  * (1 length, 2 indptr range, 3 page id range, 4 page shared).  Synchronises `stream`.  The
- * uniqueness check uses `scratch` (device, >= num_pages int32, overwritten). */
+ * check uses `scratch` (device, >= num_pages + 2 int32, overwritten): a page-owner table and
+ * the device-side report. */
 l4_status l4_decode_validate(const l4_decode_params* p, const int32_t* kv_len, const int32_t* page_indptr,
                              const int32_t* page_indices, int64_t total_pages, int64_t num_pages,
                              int32_t* scratch, int32_t* report, void* stream);

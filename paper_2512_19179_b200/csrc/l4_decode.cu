@@ -1627,10 +1627,9 @@ extern "C" l4_status l4_decode_validate(const l4_decode_params* p, const int32_t
   L4_CHECK_ARG(kv_len && page_indptr && scratch, "kv_len / page_indptr / scratch is NULL");
   L4_CHECK_ARG(total_pages == 0 || page_indices, "page_indices is NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int* d_report = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_report), 2 * sizeof(int), st);
-  const int init[2] = {0, INT_MAX};
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_report, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  int* d_report = scratch + num_pages;  // [count, min(request << 3 | kind)] after the owner table
+  static const int init[2] = {0, INT_MAX};
+  cudaError_t e = cudaMemcpyAsync(d_report, init, sizeof(init), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0xff, (size_t)num_pages * sizeof(int), st);
   if (e == cudaSuccess) {
     const int threads = 256, blocks = (int)((p->batch * 32LL + threads - 1) / threads);
@@ -1640,7 +1639,6 @@ extern "C" l4_status l4_decode_validate(const l4_decode_params* p, const int32_t
   }
   int h[2] = {0, INT_MAX};
   if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_report, sizeof(h), cudaMemcpyDeviceToHost, st);
-  if (d_report) cudaFreeAsync(d_report, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     set_error("l4_decode_validate: %s", cudaGetErrorString(e));

@@ -280,7 +280,7 @@ def validate(params: DecodeParams, kv_len, page_indptr, page_indices, num_pages:
     _need(kv_len, torch.int32, "kv_len")
     _need(page_indptr, torch.int32, "page_indptr")
     _need(page_indices, torch.int32, "page_indices")
-    scratch = torch.empty(max(int(num_pages), 1), dtype=torch.int32, device=kv_len.device)
+    scratch = torch.empty(max(int(num_pages), 1) + 2, dtype=torch.int32, device=kv_len.device)
     rep = (ctypes.c_int32 * 3)()
     _check(lib().l4_decode_validate(ctypes.byref(params), _ptr(kv_len), _ptr(page_indptr), _ptr(page_indices),
                                     int(page_indices.numel()), int(num_pages), _ptr(scratch), rep,
