@@ -7,26 +7,30 @@
 // tokens of kv head h/G, plus the natural-log LSE.
 //
 // How (B200 design):
-//  a1  plan_kernel (1 CTA): pages -> chunk size C -> near-equal splits of the
-//      requests longer than 2C -> work items binned by split length, longest
-//      bin first (LPT order), so the longest request's splits start first and
-//      short requests fill the tail (the paper's inter-SM imbalance and
-//      partitioning inefficiency).  Zeroes the split counters and
-//      the dynamic scheduler.
+//  a1  plan_core: pages -> chunk size C -> near-equal splits of the requests
+//      longer than 2C -> work items binned by split length, longest bin first
+//      (LPT order), so the longest request's splits start first and short
+//      requests fill the tail (the paper's inter-SM imbalance and partitioning
+//      inefficiency).  Run by EVERY CTA of the single-launch path
+//      (l4_decode_attention: the plan stays in shared memory, no planner launch)
+//      or by plan_kernel (l4_decode_plan: a materialised work list reused by
+//      l4_decode_run, e.g. for every layer of a step).
 //  a2  decode_kernel (persistent, 1 producer + 4 consumer warps per CTA,
 //      2 CTAs per SM): items are handed out dynamically (first one static,
-//      then an atomic ticket), so CTAs that finish early take the next-largest
-//      item.  The producer warp streams each (page, kv head) K and V slice
-//      (4 KB each, HND layout) with one TMA each (cp.async.bulk.tensor, 128B
-//      swizzle, L2 evict-first) into an 8-stage shared-memory ring tracked by
-//      mbarriers; consumer warps compute S^T = K Q^T and O^T += V^T P^T with
-//      mma.sync m16n8k16 (tokens / head_dim on M, the G <= 8 query heads on N,
-//      so GQA group 8 has no padding), an online softmax with warp-shuffle max
-//      reductions in the exp2 domain, and P split into bf16 hi + lo (Z23).
+//      then atomic tickets issued one item ahead), so CTAs that finish early
+//      take the next-largest item.  The producer warp streams each (page, kv
+//      head) K and V slice (4 KB each, HND layout) with one TMA each
+//      (cp.async.bulk.tensor, 128B swizzle, L2 evict-first) into an 8-stage
+//      shared-memory ring tracked by mbarriers; consumer warps compute
+//      S^T = K Q^T and O^T += V^T P^T with mma.sync m16n8k16 (tokens / head_dim
+//      on M, the G <= 8 query heads on N, so GQA group 8 has no padding), an
+//      online softmax with warp-shuffle max reductions in the exp2 domain, and
+//      P split into bf16 hi + lo (Z23).  With L4_DECODE_EARLY_INPUTS the next
+//      call plans and streams its first item while this one finishes (PDL).
 //  a3  LSE combine: the 4 warps of a CTA merge their (m, l, O) in shared
-//      memory; a split item writes (O/l, lse) to the workspace and the last
-//      split of (b, kv head) to finish (acq_rel atomic ticket) combines all
-//      splits (FlashDecoding aggregation) — no second launch.
+//      memory; a split item writes (O/l, lse) to the workspace; the last split
+//      of each group of 16 combines the group, the last group combines the
+//      groups (FlashDecoding aggregation) — no second launch.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
