@@ -212,17 +212,23 @@ def time_steps(wl: Workload, steps: int, warmup: int, mode: str = "early"):
     return total, None, l4.plan_info(ws)
 
 
-def time_e2e(wl: Workload, steps: int, warmup: int):
+def time_e2e(wl: Workload, steps: int, warmup: int, n_streams: int = 2, out_bf16: bool = False):
     """Same metric through the public API with HOST buffers.  Every step copies its inputs
     (q, kv_len, indptr, indices: packed in one pinned host buffer, one H2D copy) to the device,
     runs l4_decode_attention and copies the fp32 output back (one D2H copy).  Copies run on
-    their own streams, double-buffered, so step i+1's H2D and step i-1's D2H overlap step i's
-    kernel (what a serving loop does); the timed region spans the first H2D to the last D2H."""
+    their own streams and everything is double-buffered (inputs, outputs, workspaces, and two
+    compute streams), so step i+1's H2D, step i's kernel and step i-1's D2H overlap, and
+    consecutive kernels (on alternating streams) overlap each other's tail and head, as in a
+    pipelined serving loop; the timed region spans the first H2D to the last D2H."""
     import torch
     from paper_2512_19179_b200 import l4 as _l4
-    l4, params, ws0 = make_l4(wl, flags=_l4.L4_DECODE_EARLY_INPUTS)
+    from paper_2512_19179_b200 import l4 as l4m
+    l4, params, ws0 = make_l4(wl)
+    if out_bf16:
+        params = l4m.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, out_dtype=l4m.L4_DT_BF16)
     ws = [ws0, torch.zeros_like(ws0)]
-    s_h2d, s_cmp, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    s_cmps = [torch.cuda.Stream() for _ in range(n_streams)]
     parts = [wl.q, wl.kv_len, wl.indptr, wl.indices]
     offs, off = [], 0
     for t in parts:
@@ -241,19 +247,21 @@ def time_e2e(wl: Workload, steps: int, warmup: int):
             out.append(buf[o:o + nb].view(t.dtype).view(t.shape))
         return out
     d_in = [views(d) for d in d_pack]
-    d_out = [torch.empty_like(wl.out) for _ in range(2)]
+    odt = torch.bfloat16 if out_bf16 else torch.float32
+    d_out = [torch.empty(wl.out.shape, dtype=odt, device="cuda") for _ in range(2)]
     d_lse = [torch.empty_like(wl.lse) for _ in range(2)]
-    h_out = [torch.empty(wl.out.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+    h_out = [torch.empty(wl.out.shape, dtype=odt).pin_memory() for _ in range(2)]
     h2d = sum(t.numel() * t.element_size() for t in parts)
     d2h = h_out[0].numel() * h_out[0].element_size()
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_cmp = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
     for e in ev_cmp + ev_out:
-        e.record(s_cmp)
+        e.record(s_cmps[0])
 
     def step(i):
         b = i % 2
+        s_cmp = s_cmps[i % n_streams]
         with torch.cuda.stream(s_h2d):
             s_h2d.wait_event(ev_cmp[b])            # step i-2 finished reading these inputs
             d_pack[b].copy_(h_pack, non_blocking=True)
@@ -770,7 +778,7 @@ def main():
     launch_avg = total_ms / args.steps
     run_avg = run_ms / args.steps
     achieved = wl.bytes_algo / (launch_avg / 1e3) / 1e9
-    e2e_ms, h2d, d2h = time_e2e(wl, max(3, args.steps // 2), 2)
+    e2e_ms, h2d, d2h = time_e2e(wl, max(3, args.steps // 2), max(5, args.warmup))
     e2e_step = e2e_ms / max(3, args.steps // 2)
     extra = {}
     if rank == 0 and ws == 1 and not args.no_extra:
