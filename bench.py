@@ -556,8 +556,7 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         if B > 0:
-            d_len = torch.from_numpy(kv_len).pin_memory().to(device, non_blocking=True)
-            d_ptr = torch.from_numpy(indptr).pin_memory().to(device, non_blocking=True)
+            d_len, d_ptr = rt.ops.h2d.put(kv_len, indptr)
             params = l4.make_params(B, shape.num_q_heads, shape.num_kv_heads)
             l4.attention_call(params, q[:B], pool["k"], pool["v"], d_ptr, rt.table, d_len, int(rt.table.numel()),
                               out[:B], lse[:B], ws)

@@ -513,6 +513,43 @@ class RankRuntime:
                 self._add(rid, self.ops.alloc(self.pool, -(-L // PAGE)))   # prefill not emulated
 
 
+class H2DRing:
+    """Small per-step host->device copies without per-step pinned allocations: a ring of
+    preallocated pinned host buffers and device buffers; several int32 arrays are packed into
+    one slot and moved with one async copy on the current stream.  A slot is reused only after
+    its previous copy completed (event).  Arrays larger than a slot take the plain path."""
+
+    def __init__(self, device, slot_bytes: int = 1 << 20, depth: int = 4):
+        import torch
+        self.torch, self.device, self.slot_bytes, self.depth = torch, device, slot_bytes, depth
+        self.h = [torch.empty(slot_bytes, dtype=torch.uint8).pin_memory() for _ in range(depth)]
+        self.d = [torch.empty(slot_bytes, dtype=torch.uint8, device=device) for _ in range(depth)]
+        self.ev = [None] * depth
+        self.i = 0
+
+    def put(self, *arrays):
+        torch = self.torch
+        arrays = [np.ascontiguousarray(a, dtype=np.int32) for a in arrays]
+        offs, off = [], 0
+        for a in arrays:
+            offs.append(off)
+            off += (a.nbytes + 255) // 256 * 256
+        if off > self.slot_bytes:
+            return [torch.from_numpy(a).to(self.device) for a in arrays]
+        k = self.i % self.depth
+        self.i += 1
+        if self.ev[k] is not None:
+            self.ev[k].synchronize()
+        hv = self.h[k].numpy()
+        for a, o in zip(arrays, offs):
+            hv[o:o + a.nbytes] = a.view(np.uint8)
+        self.d[k][:off].copy_(self.h[k][:off], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.ev[k] = ev
+        return [self.d[k][o:o + a.nbytes].view(torch.int32) for a, o in zip(arrays, offs)]
+
+
 class DeviceOps:
     """libl4 on CUDA: page pool (host allocator over a device KV pool), attention, and the
     KV-page transport (l4_pack_pages -> NCCL send/recv -> l4_unpack_pages)."""
@@ -522,6 +559,7 @@ class DeviceOps:
         from . import l4
         self.torch, self.l4, self.shape, self.device = torch, l4, shape, device
         self.seed = seed
+        self.h2d = H2DRing(device)
 
     def make_pool(self, num_pages):
         torch = self.torch
@@ -546,10 +584,8 @@ class DeviceOps:
 
     def table_update(self, table, pos, val):
         """Scatter this step's page-id deltas into the device block table (pinned H2D, async)."""
-        torch = self.torch
-        p = torch.from_numpy(pos).pin_memory().to(self.device, non_blocking=True)
-        v = torch.from_numpy(val).pin_memory().to(self.device, non_blocking=True)
-        table.index_copy_(0, p, v)
+        p, v = self.h2d.put(pos, val)
+        table.index_copy_(0, p.long(), v)
 
     def transfer(self, pool, sends, recvs, comm):
         """sends = [(dst rank, src page ids)], recvs = [(src rank, dst page ids)] in the global
