@@ -105,6 +105,15 @@ def test_partition_sharegpt_scale_bit_exact():
             assert got[0] == ref[0] and got[1] == ref[1]
 
 
+def test_partition_bit_exact_paper_scale_e16():
+    """The paper's planning scale (E = 16) on 10k requests: bit-exact with the oracle."""
+    I, O = synth.requests_sharegpt_like(seed=1, n=10000)
+    D = synth.roofline_qoe_d()
+    ref = op.plan_dp(I, O, 16, D, 7e11, 131072, mode=0)
+    got = l4.partition(I, O, 16, D, 7e11, 131072, mode=0)
+    assert got[0] == ref[0] and got[1] == ref[1]
+
+
 def test_partition_speed_paper_setting():
     """E = 16 over a 128K-context trace in 0.06 s; S:685 relaxes to < 1 s."""
     I, O = synth.requests_sharegpt_like(seed=1, n=10000)
