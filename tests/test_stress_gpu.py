@@ -40,7 +40,10 @@ def test_random_batches_back_to_back():
         G = int(rng.choice([1, 2, 4, 8]))
         B = int(rng.integers(1, 300))
         kind = it % 3
-        if kind == 0:
+        if it % 25 == 24:        # around the single-launch batch limit (1024): both paths
+            B = int(rng.integers(1000, 1100))
+            lens = rng.integers(0, 200, size=B)
+        elif kind == 0:
             lens = rng.integers(0, 600, size=B)
         elif kind == 1:
             lens = rng.integers(1, 40, size=B)
