@@ -289,9 +289,13 @@ l4_status l4_pack_pages(const l4_kv_view* src, const int32_t* pages, int64_t n, 
 l4_status l4_unpack_pages(const l4_kv_view* dst, const int32_t* pages, int64_t n, const void* staging,
                           void* stream);
 
-/* CUDA IPC helpers for the cross-process one-sided path (one process per GPU). */
+/* CUDA IPC helpers for the cross-process one-sided path (one process per GPU): a process
+ * exports its KV pools, a peer maps them and l4_copy_pages / l4_migrate write straight into
+ * them.  The handle names the whole device allocation containing dev_ptr; offset_out
+ * (nullable) receives dev_ptr - allocation base, to add to the pointer l4_ipc_open_handle
+ * returns (pools from a caching allocator are sub-allocations). */
 enum { L4_IPC_HANDLE_BYTES = 64 };
-l4_status l4_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */);
+l4_status l4_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */, int64_t* offset_out);
 l4_status l4_ipc_open_handle(const void* handle /* 64 bytes */, void** dev_ptr_out);
 l4_status l4_ipc_close_handle(void* dev_ptr);
 /* Enable peer access from the current device to peer_device (idempotent). */

@@ -245,8 +245,41 @@ extern "C" l4_status l4_unpack_pages(const l4_kv_view* dst, const int32_t* pages
                        static_cast<cudaStream_t>(stream));
 }
 
-extern "C" l4_status l4_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda link dependency).
+typedef int (*PFN_getAddressRange)(unsigned long long*, size_t*, unsigned long long);
+PFN_getAddressRange address_range_fn() {
+  static PFN_getAddressRange fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_getAddressRange>(p);
+    cudaGetLastError();
+  }
+  return fn;
+}
+}  // namespace
+
+extern "C" l4_status l4_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
   L4_CHECK_ARG(dev_ptr && handle_out, "NULL argument");
+  // The handle names the whole allocation that contains dev_ptr (a caching allocator such as
+  // PyTorch's sub-allocates): report dev_ptr's offset from the allocation base, which is what
+  // l4_ipc_open_handle maps in the other process.
+  int64_t off = 0;
+  if (offset_out) {
+    auto fn = address_range_fn();
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (!fn || fn(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0) {
+      set_error("cuMemGetAddressRange failed for %p", dev_ptr);
+      return L4_ERR_CUDA;
+    }
+    off = (int64_t)(reinterpret_cast<unsigned long long>(dev_ptr) - base);
+  }
   cudaIpcMemHandle_t h;
   cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
   if (e != cudaSuccess) {
@@ -256,6 +289,7 @@ extern "C" l4_status l4_ipc_get_handle(const void* dev_ptr, void* handle_out) {
   }
   static_assert(sizeof(h) == L4_IPC_HANDLE_BYTES, "IPC handle is 64 bytes");
   std::memcpy(handle_out, &h, sizeof(h));
+  if (offset_out) *offset_out = off;
   return L4_OK;
 }
 

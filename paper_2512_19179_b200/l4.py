@@ -128,7 +128,7 @@ def lib() -> ctypes.CDLL:
     L.l4_unpack_pages.restype = ctypes.c_int
     L.l4_unpack_pages.argtypes = [P(KVView), vp, i64, vp, vp]
     L.l4_ipc_get_handle.restype = ctypes.c_int
-    L.l4_ipc_get_handle.argtypes = [vp, vp]
+    L.l4_ipc_get_handle.argtypes = [vp, vp, P(i64)]
     L.l4_ipc_open_handle.restype = ctypes.c_int
     L.l4_ipc_open_handle.argtypes = [vp, P(vp)]
     L.l4_ipc_close_handle.restype = ctypes.c_int
@@ -459,10 +459,12 @@ def unpack_pages(dst: KVView, pages, staging, stream=None) -> None:
                                  _stream_handle(stream)))
 
 
-def ipc_get_handle(ptr: int) -> bytes:
+def ipc_get_handle(ptr: int):
+    """(64-byte handle of the allocation containing ptr, ptr's offset in it)."""
     buf = ctypes.create_string_buffer(64)
-    _check(lib().l4_ipc_get_handle(ptr, buf))
-    return buf.raw
+    off = ctypes.c_int64(0)
+    _check(lib().l4_ipc_get_handle(ptr, buf, ctypes.byref(off)))
+    return buf.raw, int(off.value)
 
 
 def ipc_open_handle(handle: bytes) -> int:
