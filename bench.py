@@ -532,6 +532,10 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
                               policy=policy, rebalance_every=rebalance_every)
     budget_pages = sim.token_budget // 16 * 5 // 4 + 2 * sim.batch_cap
     rt = pipeline.RankRuntime(sim, rank, budget_pages, shape, pipeline.DeviceOps(shape, device, seed + rank))
+    if os.environ.get("L4_PIPE_TRANSPORT", "nccl") == "ipc" and world > 1:
+        # one-sided transport: peers' pools mapped through CUDA IPC, metadata over a CPU group
+        cpu_group = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None
+        rt.ops.setup_ipc(rt.pool, rank, world, cpu_group)
     cap = sim.batch_cap
     g = torch.Generator(device=device).manual_seed(seed + 100 + rank)
     q = torch.randn(cap, shape.num_q_heads, 128, device=device, generator=g).to(torch.bfloat16)
@@ -585,6 +589,8 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
     for k_ in ("precopy_pages", "stop_pages", "single_pages"):
         tot[k_] = rt.stats[k_]
     tot["fingerprint"] = sim.fingerprint()
+    if hasattr(rt.ops, "close_ipc"):
+        rt.ops.close_ipc()
     tot["stage_cv"] = sim.stage_cv()
     tot["stages"] = stages
     return tot

@@ -498,7 +498,7 @@ class RankRuntime:
                 pages = pages + self.ops.alloc(self.pool, need - len(pages))
                 recvs.append((src, pages[first:need]))
                 done_in.append((rid, pages))
-        nbytes = self.ops.transfer(self.pool, sends, recvs, comm)
+        nbytes = self.ops.transfer(self.pool, sends, recvs, comm, any_transfer=bool(ev.precopies or ev.migrations))
         for rid, pages in done_in:
             self._add(rid, pages)
         for pages in done_out:
@@ -587,11 +587,70 @@ class DeviceOps:
         p, v = self.h2d.put(pos, val)
         table.index_copy_(0, p.long(), v)
 
-    def transfer(self, pool, sends, recvs, comm):
+    # ---------------------------------------------------------------- one-sided (CUDA IPC)
+    def setup_ipc(self, pool, rank: int, world: int, group=None):
+        """Map every peer's KV pools into this process (CUDA IPC; handles + offsets travel over
+        the CPU process group `group`).  Afterwards transfer() pushes pages one-sidedly."""
+        import torch.distributed as dist
+        l4 = self.l4
+        hk, ok = l4.ipc_get_handle(pool["k"].data_ptr())
+        hv, ov = l4.ipc_get_handle(pool["v"].data_ptr())
+        mine = (hk, ok, hv, ov)
+        peers = [None] * world
+        dist.all_gather_object(peers, mine, group=group)
+        view = pool["view"]
+        self.ipc_group, self.ipc_rank, self.ipc_views, self.ipc_bases = group, rank, {}, []
+        for r, (pk, pok, pv, pov) in enumerate(peers):
+            if r == rank:
+                continue
+            bk, bv = l4.ipc_open_handle(pk), l4.ipc_open_handle(pv)
+            self.ipc_bases += [bk, bv]
+            self.ipc_views[r] = l4.kv_view(None, None, device=view.device, num_layers=view.num_layers,
+                                           num_pages=view.num_pages, layer_stride_bytes=view.layer_stride_bytes,
+                                           page_bytes=view.page_bytes, k_ptr=bk + pok, v_ptr=bv + pov)
+
+    def close_ipc(self):
+        for b in getattr(self, "ipc_bases", []):
+            self.l4.ipc_close_handle(b)
+        self.ipc_bases, self.ipc_views = [], {}
+
+    def _transfer_ipc(self, pool, sends, recvs, any_transfer):
+        """One-sided: the receivers' destination page lists (allocated in their idle slots)
+        reach the senders over the CPU group; each sender writes its pages straight into the
+        receiver's pool (l4_copy_pages over the IPC mapping; NVLink across GPUs), then a
+        barrier publishes them.  Every rank takes part whenever any rank transfers."""
+        import torch.distributed as dist
+        if not any_transfer:
+            return 0
+        lists = [None] * dist.get_world_size(self.ipc_group)
+        dist.all_gather_object(lists, [(src, list(pages)) for src, pages in recvs], group=self.ipc_group)
+        me = self.ipc_rank
+        queue = {}  # (sender, receiver) -> receiver's destination lists, in event order
+        for r, lst in enumerate(lists):
+            for src, pages in lst:
+                queue.setdefault((src, r), []).append(pages)
+        pb = pool["view"].page_bytes
+        nbytes = 0
+        for dst, pages in sends:
+            dpages = queue[(me, dst)].pop(0)
+            assert len(dpages) == len(pages)
+            if pages:
+                self.l4.copy_pages(pool["view"], pages, self.ipc_views[dst], dpages)
+            nbytes += len(pages) * 2 * pb
+        nbytes += sum(len(p) for _, p in recvs) * 2 * pb
+        self.torch.cuda.current_stream().synchronize()   # the pushes have landed
+        dist.barrier(group=self.ipc_group)
+        return nbytes
+
+    def transfer(self, pool, sends, recvs, comm, any_transfer=None):
         """sends = [(dst rank, src page ids)], recvs = [(src rank, dst page ids)] in the global
         event order: pack -> batched NCCL P2P -> unpack straight into the receiver's pages
-        (allocated by the caller in idle slots).  Returns bytes moved by this rank."""
+        (allocated by the caller in idle slots), or the one-sided IPC push after
+        setup_ipc().  Returns bytes moved by this rank."""
         torch, l4, dist = self.torch, self.l4, comm
+        if getattr(self, "ipc_views", None) is not None and hasattr(self, "ipc_rank"):
+            return self._transfer_ipc(pool, sends, recvs,
+                                      any_transfer if any_transfer is not None else bool(sends or recvs))
         if not sends and not recvs:
             return 0
         pb = pool["view"].page_bytes

@@ -64,7 +64,7 @@ class MockOps:
     def free(self, pool, pages):
         pool["alloc"].free(pages)
 
-    def transfer(self, pool, sends, recvs, comm):
+    def transfer(self, pool, sends, recvs, comm, any_transfer=None):
         ops, bufs, nbytes = [], [], 0
         for dst, pages in sends:
             idx = torch.tensor(pages, dtype=torch.long)
