@@ -659,7 +659,10 @@ def pipeline_line(args, world, rank, local):
                    f"{256} resident requests per instance, 1.2M-token KV budget per instance",
                    "stages": l4r["stages"], "partition_objective": obj, "qoe_d": list(qoe_d) if qoe_d else None,
                    "qoe_d_source": qoe_src,
-                   "parallelism": f"length-aware pipeline over {world} GPUs (l4_partition); KV migration over NCCL P2P",
+                   "parallelism": f"length-aware pipeline over {world} GPUs (l4_partition); KV migration "
+                                  + ("one-sided over CUDA IPC (l4_copy_pages into peers' pools)"
+                                     if os.environ.get("L4_PIPE_TRANSPORT", "nccl") == "ipc"
+                                     else "over NCCL P2P (l4_pack_pages / l4_unpack_pages)"),
                    "l2": "inputs larger than L2; no flush"},
         "tokens_per_s": round(l4r["tokens_per_s"], 1),
         "pct_hbm_peak": round(100.0 * l4r["kv_gbs"] / (world * peak), 2),
