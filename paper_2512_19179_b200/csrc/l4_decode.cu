@@ -27,6 +27,11 @@
 //      online softmax with warp-shuffle max reductions in the exp2 domain, and
 //      P split into bf16 hi + lo (Z23).  With L4_DECODE_EARLY_INPUTS the next
 //      call plans and streams its first item while this one finishes (PDL).
+//      Quad units: when the short unsplit items at the end of the LPT order
+//      are numerous (>= 4 per CTA per group of four, G <= 4), they are handed
+//      out four at a time, one whole item per consumer warp (pages of the four
+//      items interleaved in the ring), with no cross-warp merge or CTA barrier
+//      per item: short-request batches stop paying a merge per few pages.
 //  a3  LSE combine: the 4 warps of a CTA merge their (m, l, O) in shared
 //      memory; a split item writes (O/l, lse) to the workspace; the last split
 //      of each group of 16 combines the group, the last group combines the
@@ -71,6 +76,24 @@ constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
 constexpr int kNumBins = 32;
+// Warp-item ("quad") units: unsplit items of at most 2^kQuadBin - 1 pages are scheduled four at
+// a time, one whole item per consumer warp (no cross-warp merge, no CTA barrier per item).
+// 0 disables them.  Only for G <= 4 (the per-slot Q rows of four items must fit 2 CTAs/SM).
+#ifndef L4_QUAD_BIN
+#define L4_QUAD_BIN 6
+#endif
+constexpr int kQuadBin = L4_QUAD_BIN;
+static_assert(kQuadBin >= 0 && kQuadBin <= 6, "quad items hold at most 63 page ids (two per lane)");
+constexpr int kQuadMaxG = 4;
+constexpr int kQuad = 4;  // items per quad unit = consumer warps
+#ifndef L4_QUAD_TAIL
+#define L4_QUAD_TAIL 0
+#endif
+constexpr int kQuadTailPerCta = L4_QUAD_TAIL;  // CTA-wide items per CTA at the end of the quad suffix
+#ifndef L4_QUAD_MIN
+#define L4_QUAD_MIN 4
+#endif
+constexpr int kQuadMinPerCta = L4_QUAD_MIN;  // quads only if there are at least this many per CTA
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kLog2e = 1.44269504088896340736f;
 
@@ -106,7 +129,7 @@ __device__ __forceinline__ unsigned long long trace_now() {
 // Header region (256 B): plan summary + dynamic scheduler state.
 struct __align__(16) PlanHeader {
   int n_items, chunk, num_ctas, max_splits;
-  int batch, num_kv_heads, items_cap, pad;
+  int batch, num_kv_heads, items_cap, n_wide;  // n_wide: items before the quad units
   int tail_requests, tail_chunk, pad2[6];
   int sched_next, sched_done, pad3[14];  // ticket counter and finished-CTA count (self-resetting)
 };
@@ -204,7 +227,7 @@ int items_cap_for(const l4_decode_params* p, int64_t max_total_pages, int num_ct
 struct PlanArgs {
   const int* kv_len;
   const int* indptr;
-  int B, Hkv, num_ctas, forced_chunk, items_cap;
+  int B, Hkv, num_ctas, forced_chunk, items_cap, quad_bin;
   PlanHeader* header;
   WorkItem* items;
   int* counters;
@@ -270,7 +293,8 @@ constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWa
 // whatever B is.
 __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict__ indptr, int B, int Hkv,
                           int num_ctas, int forced_chunk, int items_cap, int* s_len, int* s_ptr, int* s_rb,
-                          int* s_off, unsigned char* scratch, int* C_out, int* N_out, int* Pmax_out) {
+                          int* s_off, unsigned char* scratch, int* C_out, int* N_out, int* Pmax_out,
+                          int quad_bin, int* Wide_out) {
   long long* s_ll = reinterpret_cast<long long*>(scratch);
   int* s_i = reinterpret_cast<int*>(scratch + 32 * 8);
   unsigned* s_u = reinterpret_cast<unsigned*>(scratch + 32 * 8 + 36 * 4);
@@ -344,6 +368,10 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     __syncthreads();
   }
   if (tid == 0) L4_MARK(7);
+  // Quad bins: every item of bins <= quad_bin must be unsplit.  A split request (> 2C pages,
+  // ceil(pages / C) splits) has a largest split of more than 2C/3 pages, so bins whose items have
+  // at most 2C/3 pages (2^bin - 1 <= floor(2C/3)) hold unsplit requests only.
+  if (quad_bin > 0) quad_bin = min(quad_bin, 31 - __clz((2 * C) / 3 + 1));
   if (warp == 0) {  // bases: bins in descending order, then warps in request order
     const int bin = kNumBins - 1 - lane;
     int tot = 0;
@@ -355,6 +383,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
       if (lane >= o) incl += t;
     }
     int base = incl - tot;
+    if (bin == quad_bin) s_i[34] = base;  // first rank of the quad bins (bins <= quad_bin)
     for (int w = 0; w < nw; ++w) {
       const int c = s_wcnt[w * kNumBins + bin];
       s_wcnt[w * kNumBins + bin] = base;
@@ -416,6 +445,8 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   *C_out = C;
   *N_out = (int)N;
   *Pmax_out = Pmax;
+  // items before the first quad-bin rank run CTA-wide; the rest are grouped four per unit
+  *Wide_out = (quad_bin > 0 && s_i[34] < B) ? s_off[s_i[34]] : (int)N;
 }
 
 // Work item `i` of the plan held in shared memory (fused path) — the same item plan_kernel
@@ -463,9 +494,9 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
   int* s_rb = s_ptr + Bs;
   int* s_off = s_rb + Bs;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  int C, N, Pmax;
+  int C, N, Pmax, Nw;
   plan_core(a.kv_len, a.indptr, a.B, a.Hkv, a.num_ctas, a.forced_chunk, a.items_cap, s_len, s_ptr, s_rb, s_off,
-            scratch, &C, &N, &Pmax);
+            scratch, &C, &N, &Pmax, a.quad_bin, &Nw);
   // ---- items: one thread per (request rank, kv head) writes that pair's splits
   for (int x = tid; x < a.B * a.Hkv; x += nthr) {
     const int r = x / a.Hkv, h = x - r * a.Hkv;
@@ -495,6 +526,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     hd.batch = a.B;
     hd.num_kv_heads = a.Hkv;
     hd.items_cap = a.items_cap;
+    hd.n_wide = Nw;
     hd.sched_next = 0;
     hd.sched_done = 0;
     *a.header = hd;
@@ -520,12 +552,15 @@ struct RunArgs {
   const int* kv_len;
   const int* indptr;
   int B, forced_chunk, items_cap;
+  int quad_bin;  // kQuadBin for G <= 4, else 0 (no quad units)
   int early;  // L4_DECODE_EARLY_INPUTS: read inputs before griddepcontrol.wait (fused path)
 };
 
-struct __align__(16) SlotItem {  // item handed from the producer to the consumers
-  WorkItem it;
-  int idx, pad[3];
+struct __align__(16) SlotItem {  // unit handed from the producer to the consumers
+  WorkItem it[kQuad];  // CTA-wide unit: it[0]; quad unit: one item per consumer warp
+  int idx;             // work-item index of it[0] (partial slot of a split item)
+  int nsub;            // 0: CTA-wide unit (it[0].b < 0: no more work); 1..4: quad unit
+  int maxnp, pad;      // quad: pages of its longest item
 };
 
 constexpr int kCombineScratchBytes = (kMaxCombine * kMaxG + 2 * kMaxG) * 4 + kConsumerThreads * 16;
@@ -548,7 +583,8 @@ constexpr int align16c(int x) { return (x + 15) & ~15; }
 template <int G>
 struct SmemLayout {
   static constexpr int stages_n = G == 8 ? 8 : L4_STAGES_SMALL_G;
-  static constexpr int qslot_bytes = G * kHeadDim * 2;
+  static constexpr bool quads = kQuadBin > 0 && G <= kQuadMaxG;
+  static constexpr int qslot_bytes = (quads ? kQuad : 1) * G * kHeadDim * 2;  // Q rows of one unit
   static constexpr int merge_bytes =
       align16c(cmax(kConsumerWarps * G * kMergeStride * 4, cmax(kPlanScratchBytes, kCombineScratchBytes)));
   static constexpr int stages = 0;
@@ -561,7 +597,10 @@ struct SmemLayout {
   static constexpr int nbars = 2 * stages_n + 2 * kItemSlots;
   static constexpr int seq = bars + nbars * 8;  // int [stages_n]: page sequence number armed per stage
   static constexpr int flag = seq + stages_n * 4;
-  static constexpr int total = align16c(flag + 16);
+#ifndef L4_SMEM_PAD
+#define L4_SMEM_PAD 0
+#endif
+  static constexpr int total = align16c(flag + 16) + (G <= 4 ? L4_SMEM_PAD : 0);  // pad: development experiments only
   static constexpr int alloc = total + 1024;  // room to align the base to 1024 B (128B swizzle)
   static_assert(merge_o % 16 == 0 && total % 16 == 0 && bars % 8 == 0, "aligned areas");
 };
@@ -856,7 +895,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     raw_t1 = atomicAdd(&a.header->sched_next, 1);
     raw_t2 = atomicAdd(&a.header->sched_next, 1);
   }
-  int n_items, plan_C = 0;
+  int n_items, plan_C = 0, n_wide;
   int *p_len = nullptr, *p_ptr = nullptr, *p_rb = nullptr, *p_off = nullptr;
   if constexpr (kFused) {
     // a1 in every CTA: the plan lives in this CTA's shared memory (scratch in the merge area,
@@ -867,10 +906,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     p_off = p_rb + a.B;
     int pmax;
     plan_core(a.kv_len, a.indptr, a.B, a.Hkv, W, a.forced_chunk, a.items_cap, p_len, p_ptr, p_rb, p_off,
-              smem + SL::merge_o, &plan_C, &n_items, &pmax);
+              smem + SL::merge_o, &plan_C, &n_items, &pmax, SL::quads ? a.quad_bin : 0, &n_wide);
   } else {
     n_items = a.header->n_items;
+    n_wide = SL::quads ? a.header->n_wide : n_items;
   }
+  // Scheduling units: items [0, n_wide) one per unit (CTA-wide); then the quad-eligible suffix
+  // four items per unit (one per consumer warp), except its last kQuadTailPerCta x W items,
+  // which run CTA-wide again so the end of the launch has the fine granularity of single
+  // items.  Quads only when every CTA gets several (a small batch keeps 4 warps per item: one
+  // warp alone streams a page at a fraction of a CTA's share of HBM bandwidth).
+  const int q_rest = n_items - n_wide;
+  int n_quads = (q_rest - min(q_rest, kQuadTailPerCta * W)) / kQuad;
+  if (n_quads < kQuadMinPerCta * W) n_quads = 0;
+  const int n_units = n_items - (kQuad - 1) * n_quads;
+  const int u_tail = n_wide + n_quads;  // first tail unit
   if (threadIdx.x == 0) L4_MARK(2);
   auto get_item = [&](int i) -> WorkItem {
     if constexpr (kFused)
@@ -878,6 +928,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     else
       return load_item(a.items, i, n_items);
   };
+  auto unit_item = [&](int u) -> int {
+    return u < n_wide ? u : (u < u_tail ? n_wide + kQuad * (u - n_wide) : u + (kQuad - 1) * n_quads);
+  };
+  auto is_quad = [&](int u) -> bool { return u >= n_wide && u < u_tail; };
 
   if (warp == kConsumerWarps) {
     // ============================== producer warp: items, Q and KV pages via TMA
@@ -894,10 +948,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     // resets the scheduler for the next run.
     auto resolve = [&](int raw) -> int {
       const int t = __shfl_sync(0xffffffffu, raw, 0);
-      if (t < 0 || exhausted) return n_items;
-      if (W + t >= n_items) {
+      if (t < 0 || exhausted) return n_units;
+      if (W + t >= n_units) {
         exhausted = true;
-        return n_items;
+        return n_units;
       }
       return W + t;
     };
@@ -909,10 +963,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     auto post_item = [&](uint32_t kk, const WorkItem& it, int idx) {  // lane 0: item + its Q rows
       const uint32_t slot = kk % kItemSlots;
       mbar_wait(bar_iempty + slot * 8, ((kk / kItemSlots) & 1) ^ 1);
-      SlotItem si;
-      si.it = it;
-      si.idx = idx;
-      s_items[slot] = si;
+      s_items[slot].it[0] = it;
+      s_items[slot].idx = idx;
+      s_items[slot].nsub = 0;
       const uint32_t qbytes = G * kHeadDim * 2;
       mbar_arrive_expect_tx(bar_ifull + slot * 8, qbytes);
       bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes,
@@ -940,16 +993,77 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (qseq == 0) L4_MARK(3);
 #endif
     };
+    auto issue_null = [&]() {  // lane 0: a stage with no data (a quad's shorter item)
+      const uint32_t st = qseq % kStages;
+      mbar_wait(bar_empty + st * 8, ((qseq / kStages) & 1) ^ 1);
+      if constexpr (kStages % kConsumerWarps != 0) st_release_cta(sbase + SL::seq + st * 4, (int)qseq);
+      mbar_arrive(bar_full + st * 8);
+    };
+    // Quad unit u (items f .. f + nsub - 1, one per consumer warp): lane w < nsub posts item w
+    // and its Q rows; page j of item w goes out as ring page qbase + 4 j + w (null stages pad
+    // the shorter items), so warp w always owns the ring pages = w (mod 4) of the unit.
+    auto issue_quad = [&](int u, uint32_t kk) {
+      if constexpr (SL::quads) {
+        const int f = unit_item(u);
+        const int nsub = kQuad;  // quad units are always full (the remainder runs CTA-wide)
+        const WorkItem my = get_item(f + min(lane & (kQuad - 1), nsub - 1));
+        int npw[kQuad], hw[kQuad], ids[kQuad][2];  // page ids j = lane and j = 32 + lane
+        int maxnp = 0;
+#pragma unroll
+        for (int w = 0; w < kQuad; ++w) {
+          const int n = __shfl_sync(0xffffffffu, my.pend - my.pbeg, w);
+          const int pb = __shfl_sync(0xffffffffu, my.pbeg, w);
+          hw[w] = __shfl_sync(0xffffffffu, my.h, w);
+          npw[w] = w < nsub ? n : 0;
+          ids[w][0] = lane < npw[w] ? __ldg(a.indices + pb + lane) : 0;
+          ids[w][1] = lane + 32 < npw[w] ? __ldg(a.indices + pb + 32 + lane) : 0;
+          maxnp = max(maxnp, npw[w]);
+        }
+        const uint32_t slot = kk % kItemSlots;
+        if (lane == 0) mbar_wait(bar_iempty + slot * 8, ((kk / kItemSlots) & 1) ^ 1);
+        __syncwarp();
+        if (lane < nsub) s_items[slot].it[lane] = my;
+        if (lane == 0) {
+          s_items[slot].idx = f;
+          s_items[slot].nsub = nsub;
+          s_items[slot].maxnp = maxnp;
+        }
+        __syncwarp();
+        const uint32_t qbytes = G * kHeadDim * 2;
+        if (lane == 0) mbar_arrive_expect_tx(bar_ifull + slot * 8, nsub * qbytes);
+        __syncwarp();
+        if (lane < nsub)
+          bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes + lane * qbytes,
+                    a.q + ((size_t)my.b * a.Hq + (size_t)my.h * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
+        for (int j = 0; j < maxnp; ++j) {
+#pragma unroll
+          for (int w = 0; w < kQuad; ++w) {
+            const int page = __shfl_sync(0xffffffffu, j < 32 ? ids[w][0] : ids[w][1], j & 31);
+            if (lane == 0) {
+              if (j < npw[w])
+                issue_page(page, hw[w]);
+              else
+                issue_null();
+            }
+            ++qseq;
+          }
+        }
+      }
+    };
     // The first item (blockIdx.x: no ticket needed) goes out before anything else: its Q and
     // its first kStages pages (early mode: all its pages, which may run while the previous
     // kernel finishes) are in flight while the scheduler tickets resolve.
-    int i_cur = blockIdx.x < n_items ? (int)blockIdx.x : n_items;
-    if (i_cur >= n_items) exhausted = true;
-    WorkItem cur = get_item(i_cur);
-    int cur_idx = (i_cur < n_items && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
+    int i_cur = blockIdx.x < n_units ? (int)blockIdx.x : n_units;  // unit indices from here on
+    if (i_cur >= n_units) exhausted = true;
+    WorkItem cur = get_item(unit_item(i_cur));
+    int cur_idx = (i_cur < n_units && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
     int pre = 0;
-    if (i_cur < n_items) {
-      if (lane == 0) post_item(0, cur, i_cur);
+    bool first_done = false;  // a quad first unit goes out whole before the tickets
+    if (is_quad(i_cur)) {
+      issue_quad(i_cur, 0);
+      first_done = true;
+    } else if (i_cur < n_units) {
+      if (lane == 0) post_item(0, cur, unit_item(i_cur));
       const int np0 = cur.pend - cur.pbeg;
       pre = early ? np0 : min(np0, kStages);
       int blk = cur_idx;
@@ -973,17 +1087,28 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
     int i_nxt = resolve(raw_t0);
-    WorkItem nxt = get_item(i_nxt);
+    WorkItem nxt = get_item(unit_item(i_nxt));
     int i_nn = resolve(raw_t1);
     int raw_p = raw_t2;  // resolved in iteration 0
     uint32_t k = 0;
-    for (; i_cur < n_items; ++k) {
-      // prefetch: the next item's first page ids, the item after's struct, one more ticket
-      const int nxt_idx = (i_nxt < n_items && lane < nxt.pend - nxt.pbeg) ? __ldg(a.indices + nxt.pbeg + lane) : 0;
-      const WorkItem nn = get_item(i_nn);
+    for (; i_cur < n_units; ++k) {
+      // prefetch: the next unit's first page ids, the unit after's first item, one more ticket
+      const int nxt_idx = (i_nxt < n_units && !is_quad(i_nxt) && lane < nxt.pend - nxt.pbeg)
+                              ? __ldg(a.indices + nxt.pbeg + lane) : 0;
+      const WorkItem nn = get_item(unit_item(i_nn));
       const int i_nnn = resolve(raw_p);  // issued one iteration ago
       raw_p = issue();
-      if (k > 0 && lane == 0) post_item(k, cur, i_cur);
+      if (is_quad(i_cur)) {
+        if (!(k == 0 && first_done)) issue_quad(i_cur, k);
+        i_cur = i_nxt;
+        cur = nxt;
+        cur_idx = nxt_idx;
+        i_nxt = i_nn;
+        nxt = nn;
+        i_nn = i_nnn;
+        continue;
+      }
+      if (k > 0 && lane == 0) post_item(k, cur, unit_item(i_cur));
       const int np = cur.pend - cur.pbeg;
       const int jstart = k == 0 ? pre : 0;  // item 0's first `pre` pages went out above
       if (jstart < np) {
@@ -1022,7 +1147,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0) {
       const uint32_t slot = k % kItemSlots;
       mbar_wait(bar_iempty + slot * 8, ((k / kItemSlots) & 1) ^ 1);
-      s_items[slot].it.b = -1;
+      s_items[slot].it[0].b = -1;
+      s_items[slot].nsub = 0;
       mbar_arrive(bar_ifull + slot * 8);
     }
     return;
@@ -1076,7 +1202,76 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef L4_TRACE
     if (ct == 0) trace_add(10, trace_now() - ti0);
 #endif
-    const WorkItem it = s_items[slot].it;
+    const int nsub = s_items[slot].nsub;
+    if (SL::quads && nsub > 0) {
+      // ---- quad unit: this warp runs item `warp` alone (ring pages qbase + 4 j + warp) and
+      // writes its output; no merge, no CTA barrier (warps drift freely across quad units)
+      const int maxnp = s_items[slot].maxnp;
+      const bool mine = warp < nsub;
+      const WorkItem it = s_items[slot].it[mine ? warp : 0];
+      uint32_t qf[8][2];
+      {
+        const unsigned char* qs = smem + SL::qslots + slot * SL::qslot_bytes + warp * (G * kHeadDim * 2);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          if (g < G && mine) {
+            qf[kk][0] = *reinterpret_cast<const uint32_t*>(qs + g * 256 + (kk * 16 + 2 * c) * 2);
+            qf[kk][1] = *reinterpret_cast<const uint32_t*>(qs + g * 256 + (kk * 16 + 8 + 2 * c) * 2);
+          } else {
+            qf[kk][0] = 0u;
+            qf[kk][1] = 0u;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_iempty + slot * 8);
+      float acc[8][4];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+      float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+      const int np = mine ? it.pend - it.pbeg : 0;
+      for (int j = 0; j < maxnp; ++j) {
+        const uint32_t q = qbase + kQuad * j + warp;
+        const uint32_t st = q % kStages;
+        if constexpr (kStages % kConsumerWarps != 0) {
+          while (ld_acquire_cta(sbase + SL::seq + st * 4) != (int)q) {
+          }
+        }
+        mbar_wait(bar_full + st * 8, (q / kStages) & 1);
+        if (j < np)
+          consume_page(sbase + SL::stages + st * kStageBytes, (j == np - 1) ? it.last_valid : kPage, qf, acc, mrow,
+                       lrow, a.scale_log2, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty + st * 8);
+      }
+      qbase += kQuad * maxnp;
+      if (early && k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
+      if (mine) {
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          lrow[0] += __shfl_xor_sync(0xffffffffu, lrow[0], o);
+          lrow[1] += __shfl_xor_sync(0xffffffffu, lrow[1], o);
+        }
+        const size_t row0 = (size_t)it.b * a.Hq + (size_t)it.h * G;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int head = 2 * c + hh;
+          if (head < G) {
+            const bool any = mrow[hh] != -INFINITY;
+            const float L = lrow[hh];
+            const size_t row = row0 + head;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              store_out(a, row * kHeadDim + mt * 16 + g, any ? acc[mt][hh] / L : 0.f);
+              store_out(a, row * kHeadDim + mt * 16 + g + 8, any ? acc[mt][2 + hh] / L : 0.f);
+            }
+            if (g == 0 && a.lse) a.lse[row] = any ? (mrow[hh] + __log2f(L)) * kLn2 : -INFINITY;
+          }
+        }
+      }
+      continue;
+    }
+    const WorkItem it = s_items[slot].it[0];
     const int item_idx = s_items[slot].idx;
     if (it.b < 0) break;
     uint32_t qf[8][2];
@@ -1422,6 +1617,7 @@ static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, con
   a.num_ctas = ctas;
   a.forced_chunk = p->chunk_pages;
   a.items_cap = L.items_cap;
+  a.quad_bin = G <= kQuadMaxG ? kQuadBin : 0;
   a.header = reinterpret_cast<PlanHeader*>(ws + L.header);
   a.items = reinterpret_cast<WorkItem*>(ws + L.items);
   a.counters = reinterpret_cast<int*>(ws + L.counters);
@@ -1504,6 +1700,7 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   a.B = p->batch;
   a.forced_chunk = p->chunk_pages;
   a.items_cap = L.items_cap;
+  a.quad_bin = G <= kQuadMaxG ? kQuadBin : 0;
   a.early = fused && (p->flags & L4_DECODE_EARLY_INPUTS) != 0;
   if (fused) {
     switch (G) {

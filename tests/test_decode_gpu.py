@@ -161,6 +161,8 @@ def test_plan_covers_every_token_once():
             C = info.chunk_pages
             plain_ns = 1 if npg <= 2 * C else -(-npg // C)
             sizes.append(0 if npg == 0 else -(-npg // plain_ns))
+            if plain_ns > 1:  # the quad-bin bound: a split request's largest split exceeds 2C/3
+                assert 3 * sizes[-1] > 2 * C
             # requests of <= 2C pages are split only in the guided tail, into tail chunks
             if ns != plain_ns:
                 Ct = info.tail_chunk_pages
@@ -272,6 +274,41 @@ def test_fused_equals_plan_plus_run_bitwise(G, chunk):
     for o4, l4_ in early:
         assert torch.equal(o2, o4) and torch.equal(l2, l4_)
     _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_quad_units_short_batch(G):
+    """Large batches of short requests run as quad units (four unsplit items per CTA unit, one
+    per consumer warp, no merge), with the long requests CTA-wide before them and a CTA-wide
+    tail after them.  8192 items (B = 1024, 8 kv heads) clear the >= 4 quads per CTA threshold.
+    Ragged lengths (NaN-poisoned tails), empty requests, items of 32..63 pages (the second
+    block of page ids), fp32 and bf16 outputs; fused == plan + run bitwise; early-input
+    back-to-back calls bitwise; oracle within 2e-3."""
+    rng = np.random.default_rng(300 + G)
+    lens = rng.integers(1, 1009, size=1024)
+    lens[:6] = [0, 1, 16, 1008, 513, 0]
+    lens[-3:] = [9000, 20000, 3000]  # CTA-wide items ahead of the quad suffix
+    Hkv = 8
+    table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, Hkv * G, Hkv, seed=G)
+    params = l4.make_params(table.batch, Hkv * G, Hkv)
+    ws = l4.alloc_workspace(params, table.total_pages)
+    o1, l1 = _plan_run(params, table, qd, kd, vd, ip, ix, kl, ws)
+    o2, l2 = _fused(params, table, qd, kd, vd, ip, ix, kl, ws)
+    pe = l4.make_params(table.batch, Hkv * G, Hkv, flags=l4.L4_DECODE_EARLY_INPUTS)
+    early = [_fused(pe, table, qd, kd, vd, ip, ix, kl, ws) for _ in range(3)]
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    for o4, l4_ in early:
+        assert torch.equal(o2, o4) and torch.equal(l2, l4_)
+    _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
+    pb = l4.make_params(table.batch, Hkv * G, Hkv, out_dtype=l4.L4_DT_BF16)
+    ob = torch.empty(table.batch, Hkv * G, 128, device="cuda", dtype=torch.bfloat16)
+    lb = torch.empty(table.batch, Hkv * G, device="cuda")
+    l4.attention_call(pb, qd, kd, vd, ip, ix, kl, table.total_pages, ob, lb, ws)
+    torch.cuda.synchronize()
+    # bf16 output = the fp32 result rounded once
+    assert torch.equal(ob, o2.to(torch.bfloat16))
+    assert torch.equal(lb, l2)
 
 
 def test_fused_workspace_reuse_across_batch_sizes():
