@@ -391,6 +391,9 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     }
   }
   __syncthreads();
+  // read before the barriers below: the scratch is the merge area, which consumers overwrite
+  // once their first item is done
+  const int quad_rank = s_i[34];
   if (tid == 0) L4_MARK(8);
   for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
     const int b = t0 + lane;
@@ -446,7 +449,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   *N_out = (int)N;
   *Pmax_out = Pmax;
   // items before the first quad-bin rank run CTA-wide; the rest are grouped four per unit
-  *Wide_out = (quad_bin > 0 && s_i[34] < B) ? s_off[s_i[34]] : (int)N;
+  *Wide_out = (quad_bin > 0 && quad_rank < B) ? s_off[quad_rank] : (int)N;
 }
 
 // Work item `i` of the plan held in shared memory (fused path) — the same item plan_kernel
@@ -867,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     for (int i = 0; i < kItemSlots; ++i) {
       mbar_init(bar_ifull + i * 8, 1);
-      mbar_init(bar_iempty + i * 8, kConsumerWarps);
+      mbar_init(bar_iempty + i * 8, kConsumerThreads);  // every consumer thread releases its reads
     }
     fence_mbar_init();
   }
@@ -1020,9 +1023,21 @@ __global__ void __launch_bounds__(kThreads, 2)
           maxnp = max(maxnp, npw[w]);
         }
         const uint32_t slot = kk % kItemSlots;
+        // lane 0 writes the whole slot (it waited for it and arrives on its full barrier)
+        int* fld = reinterpret_cast<int*>(&s_items[slot]);
         if (lane == 0) mbar_wait(bar_iempty + slot * 8, ((kk / kItemSlots) & 1) ^ 1);
-        __syncwarp();
-        if (lane < nsub) s_items[slot].it[lane] = my;
+#pragma unroll
+        for (int w = 0; w < kQuad; ++w) {
+          const int v0 = __shfl_sync(0xffffffffu, my.b, w), v1 = __shfl_sync(0xffffffffu, my.h, w);
+          const int v2 = __shfl_sync(0xffffffffu, my.pbeg, w), v3 = __shfl_sync(0xffffffffu, my.pend, w);
+          const int v4 = __shfl_sync(0xffffffffu, my.last_valid, w);
+          const int v5 = __shfl_sync(0xffffffffu, my.part_base, w);
+          const int v6 = __shfl_sync(0xffffffffu, my.nsplit, w), v7 = __shfl_sync(0xffffffffu, my.split, w);
+          if (lane == 0) {
+            int* d = fld + w * 8;
+            d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3; d[4] = v4; d[5] = v5; d[6] = v6; d[7] = v7;
+          }
+        }
         if (lane == 0) {
           s_items[slot].idx = f;
           s_items[slot].nsub = nsub;
@@ -1032,9 +1047,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t qbytes = G * kHeadDim * 2;
         if (lane == 0) mbar_arrive_expect_tx(bar_ifull + slot * 8, nsub * qbytes);
         __syncwarp();
-        if (lane < nsub)
-          bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes + lane * qbytes,
-                    a.q + ((size_t)my.b * a.Hq + (size_t)my.h * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
+#pragma unroll
+        for (int w = 0; w < kQuad; ++w) {  // lane 0 (the lane that waited for the slot) loads Q
+          const int qb = __shfl_sync(0xffffffffu, my.b, w), qh = __shfl_sync(0xffffffffu, my.h, w);
+          if (lane == 0 && w < nsub)
+            bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes + w * qbytes,
+                      a.q + ((size_t)qb * a.Hq + (size_t)qh * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
+        }
         for (int j = 0; j < maxnp; ++j) {
 #pragma unroll
           for (int w = 0; w < kQuad; ++w) {
@@ -1224,7 +1243,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_iempty + slot * 8);
+      mbar_arrive(bar_iempty + slot * 8);
       float acc[8][4];
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
@@ -1289,7 +1308,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(bar_iempty + slot * 8);
+    mbar_arrive(bar_iempty + slot * 8);
 
     float acc[8][4];
 #pragma unroll
