@@ -417,6 +417,21 @@ def heterogeneity_slowdown(steps: int, warmup: int):
     return out
 
 
+def short_batches(steps: int, warmup: int):
+    """Homogeneous batches of short requests at the largest single-launch batch (B = 1024,
+    Llama-3-8B shape): the per-item overheads the quad units remove."""
+    import torch
+    out = []
+    for L in (64, 200, 530):
+        w = Workload(f"short{L}", np.full(1024, L, dtype=np.int64), synth.SHAPE_LLAMA3_8B)
+        t, _, _ = time_steps(w, steps, warmup)
+        out.append(dict(length=L, batch=1024, us=round(t / steps * 1e3, 2),
+                        gbs=round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1)))
+        del w
+        torch.cuda.empty_cache()
+    return out
+
+
 def migration_bandwidth(reps: int = 10):
     """l4_migrate of one request at the Llama-3-8B shape with all 32 layers:
     a 2048-token request = 128 pages x 32 layers x (K, V) = 256 MiB.  Loopback on one GPU
@@ -818,6 +833,7 @@ def main():
     if rank == 0 and ws == 1 and not args.no_extra:
         extra = mixed_vs_binned(max(5, args.steps // 2), 3)
         extra["fig2_heterogeneity"] = heterogeneity_slowdown(max(5, args.steps // 2), 3)
+        extra["short_batches"] = short_batches(max(5, args.steps // 2), 3)
         extra["migration"] = migration_bandwidth()
         extra["partition_m6"] = partition_speed()
     cpu = None

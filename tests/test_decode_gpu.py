@@ -214,6 +214,14 @@ def _sampled_full_size(lens, shape, seed, samples):
     return err
 
 
+def test_full_size_short_stage_sampled():
+    """bench.py's stage-shaped [0, 1024) batch (B = 1024 at the Llama-3-8B shape, the short
+    stage an L4 instance serves): quad units at full size, ragged lengths around the bench's 530."""
+    lens = np.random.default_rng(530).integers(300, 761, size=1024)
+    lens[0], lens[-1] = 1, 1023
+    _sampled_full_size(lens, synth.SHAPE_LLAMA3_8B, 0, [0, 1, 511, 1022, 1023])
+
+
 def test_full_size_c2_sampled():
     lens = synth.lengths_c2()
     _sampled_full_size(lens, synth.SHAPE_LLAMA3_8B, 0, [0, 1, 124, 249])
