@@ -28,7 +28,7 @@
 //      P split into bf16 hi + lo (Z23).  With L4_DECODE_EARLY_INPUTS the next
 //      call plans and streams its first item while this one finishes (PDL).
 //      Quad units: when the short unsplit items at the end of the LPT order
-//      are numerous (>= 4 per CTA per group of four, G <= 4), they are handed
+//      are numerous (>= 4 units of four per CTA), they are handed
 //      out four at a time, one whole item per consumer warp (pages of the four
 //      items interleaved in the ring), with no cross-warp merge or CTA barrier
 //      per item: short-request batches stop paying a merge per few pages.
@@ -78,7 +78,8 @@ constexpr int kPlanThreads = 1024;
 constexpr int kNumBins = 32;
 // Warp-item ("quad") units: unsplit items of at most 2^kQuadBin - 1 pages are scheduled four at
 // a time, one whole item per consumer warp (no cross-warp merge, no CTA barrier per item).
-// 0 disables them.  Only for G <= 4 (the per-slot Q rows of four items must fit 2 CTAs/SM).
+// 0 disables them.  G <= 4: the four items' Q rows sit in the unit slot; G = 8: they travel
+// through the page ring (a 2-D TMA box each, four ring positions ahead of the pages).
 #ifndef L4_QUAD_BIN
 #define L4_QUAD_BIN 6
 #endif
@@ -586,8 +587,12 @@ constexpr int align16c(int x) { return (x + 15) & ~15; }
 template <int G>
 struct SmemLayout {
   static constexpr int stages_n = G == 8 ? 8 : L4_STAGES_SMALL_G;
-  static constexpr bool quads = kQuadBin > 0 && G <= kQuadMaxG;
-  static constexpr int qslot_bytes = (quads ? kQuad : 1) * G * kHeadDim * 2;  // Q rows of one unit
+  static constexpr bool quads = kQuadBin > 0;
+  // G <= 4: a unit slot holds the Q rows of four items (+12 KB at G = 4); G = 8: the four Q
+  // row blocks travel through the page ring instead (four ring positions ahead of the pages)
+  static constexpr bool ring_q = G > kQuadMaxG;
+  static constexpr int qslot_bytes = (quads && !ring_q ? kQuad : 1) * G * kHeadDim * 2;  // Q rows of one unit
+  static_assert(!ring_q || G * kHeadDim * 2 <= kStageBytes, "Q rows fit one ring stage");
   static constexpr int merge_bytes =
       align16c(cmax(kConsumerWarps * G * kMergeStride * 4, cmax(kPlanScratchBytes, kCombineScratchBytes)));
   static constexpr int stages = 0;
@@ -841,7 +846,8 @@ __device__ __forceinline__ WorkItem load_item(const WorkItem* items, int i, int 
 
 template <int G, bool kFused>
 __global__ void __launch_bounds__(kThreads, 2)
-    decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, RunArgs a) {
+    decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  const __grid_constant__ CUtensorMap tmQ, RunArgs a) {
   using namespace dev;
   using SL = SmemLayout<G>;
   constexpr int kStages = SL::stages_n;
@@ -877,6 +883,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kConsumerWarps && lane == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
+    if constexpr (SmemLayout<G>::quads && SmemLayout<G>::ring_q) prefetch_tmap(&tmQ);
   }
   __syncthreads();
   // PDL: the next kernel in the stream may start its prologue as CTAs of this one retire; it
@@ -1045,14 +1052,31 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncwarp();
         const uint32_t qbytes = G * kHeadDim * 2;
-        if (lane == 0) mbar_arrive_expect_tx(bar_ifull + slot * 8, nsub * qbytes);
-        __syncwarp();
+        if constexpr (SL::ring_q) {
+          // slot published without data; item w's Q rows go to ring position qbase + w
+          if (lane == 0) mbar_arrive(bar_ifull + slot * 8);
 #pragma unroll
-        for (int w = 0; w < kQuad; ++w) {  // lane 0 (the lane that waited for the slot) loads Q
-          const int qb = __shfl_sync(0xffffffffu, my.b, w), qh = __shfl_sync(0xffffffffu, my.h, w);
-          if (lane == 0 && w < nsub)
-            bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes + w * qbytes,
-                      a.q + ((size_t)qb * a.Hq + (size_t)qh * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
+          for (int w = 0; w < kQuad; ++w) {
+            const int qb = __shfl_sync(0xffffffffu, my.b, w), qh = __shfl_sync(0xffffffffu, my.h, w);
+            if (lane == 0) {
+              const uint32_t st = qseq % kStages;
+              mbar_wait(bar_empty + st * 8, ((qseq / kStages) & 1) ^ 1);
+              if constexpr (kStages % kConsumerWarps != 0) st_release_cta(sbase + SL::seq + st * 4, (int)qseq);
+              mbar_arrive_expect_tx(bar_full + st * 8, qbytes);
+              tma_load_2d(sbase + SL::stages + st * kStageBytes, &tmQ, 0, qb * a.Hq + qh * G, bar_full + st * 8);
+            }
+            ++qseq;
+          }
+        } else {
+          if (lane == 0) mbar_arrive_expect_tx(bar_ifull + slot * 8, nsub * qbytes);
+          __syncwarp();
+#pragma unroll
+          for (int w = 0; w < kQuad; ++w) {  // lane 0 (the lane that waited for the slot) loads Q
+            const int qb = __shfl_sync(0xffffffffu, my.b, w), qh = __shfl_sync(0xffffffffu, my.h, w);
+            if (lane == 0 && w < nsub)
+              bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes + w * qbytes,
+                        a.q + ((size_t)qb * a.Hq + (size_t)qh * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
+          }
         }
         for (int j = 0; j < maxnp; ++j) {
 #pragma unroll
@@ -1229,8 +1253,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const bool mine = warp < nsub;
       const WorkItem it = s_items[slot].it[mine ? warp : 0];
       uint32_t qf[8][2];
-      {
-        const unsigned char* qs = smem + SL::qslots + slot * SL::qslot_bytes + warp * (G * kHeadDim * 2);
+      auto load_qf = [&](const unsigned char* qs) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if (g < G && mine) {
@@ -1241,9 +1264,24 @@ __global__ void __launch_bounds__(kThreads, 2)
             qf[kk][1] = 0u;
           }
         }
+      };
+      if constexpr (SL::ring_q) {
+        mbar_arrive(bar_iempty + slot * 8);
+        const uint32_t q = qbase + warp, st = q % kStages;  // this warp's Q rows: ring position qbase + warp
+        if constexpr (kStages % kConsumerWarps != 0) {
+          while (ld_acquire_cta(sbase + SL::seq + st * 4) != (int)q) {
+          }
+        }
+        mbar_wait(bar_full + st * 8, (q / kStages) & 1);
+        load_qf(smem + SL::stages + st * kStageBytes);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty + st * 8);
+        qbase += kQuad;
+      } else {
+        load_qf(smem + SL::qslots + slot * SL::qslot_bytes + warp * (G * kHeadDim * 2));
+        __syncwarp();
+        mbar_arrive(bar_iempty + slot * 8);
       }
-      __syncwarp();
-      mbar_arrive(bar_iempty + slot * 8);
       float acc[8][4];
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
@@ -1474,6 +1512,23 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+// q [B, Hq, 128] bf16 as rows of 128 elements; box = G rows (no swizzle: lands as the G x 256 B
+// block the consumers read with plain shared loads).  Used by the G = 8 quad units (ring_q).
+l4_status make_qmap(CUtensorMap* tm, const void* q, int64_t rows, int G) {
+  auto enc = get_encode_fn();
+  if (!enc) return fail(L4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no device)");
+  if (rows <= 0 || rows > ((int64_t)1 << 31)) return fail(L4_ERR_INVALID_ARG, "q too large for a tensor map");
+  cuuint64_t dims[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kHeadDim * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kHeadDim, (cuuint32_t)G};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(q), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(L4_ERR_INVALID_ARG, "cuTensorMapEncodeTiled(q) failed");
+  return L4_OK;
+}
+
 // Pool [num_pages, Hkv, 16, 128] bf16 viewed as a 3-D tensor
 // (64 columns, num_pages*Hkv*16 rows of 256 B, 2 column halves 128 B apart);
 // one box = 64 x 16 x 2 = one whole (page, kv head) slice of 4 KB, landing in
@@ -1498,7 +1553,8 @@ l4_status make_tmap(CUtensorMap* tm, const void* base, int64_t rows) {
 }
 
 template <int G, bool kFused>
-l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunArgs& a, int grid, cudaStream_t st) {
+l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tq, const RunArgs& a,
+                        int grid, cudaStream_t st) {
   static bool attr_set[64] = {false};
   const size_t smem_max = SmemLayout<G>::alloc + (kFused ? fused_plan_bytes(kFusedMaxBatch) : 0);
   int dev = 0;
@@ -1526,7 +1582,7 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunA
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<G, kFused>, tk, tv, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<G, kFused>, tk, tv, tq, a);
   if (e != cudaSuccess) {
     set_error("decode_kernel launch failed: %s", cudaGetErrorString(e));
     cudaGetLastError();
@@ -1636,7 +1692,7 @@ static l4_status plan_impl(const l4_decode_params* p, const int32_t* kv_len, con
   a.num_ctas = ctas;
   a.forced_chunk = p->chunk_pages;
   a.items_cap = L.items_cap;
-  a.quad_bin = G <= kQuadMaxG ? kQuadBin : 0;
+  a.quad_bin = kQuadBin;
   a.header = reinterpret_cast<PlanHeader*>(ws + L.header);
   a.items = reinterpret_cast<WorkItem*>(ws + L.items);
   a.counters = reinterpret_cast<int*>(ws + L.counters);
@@ -1696,6 +1752,9 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   if (s != L4_OK) return s;
   s = make_tmap(&tv, v_pages, rows);
   if (s != L4_OK) return s;
+  CUtensorMap tq;  // q [B * Hq rows of 256 B]: one box = the G query rows of a kv group (2-D TMA)
+  s = make_qmap(&tq, q, (int64_t)p->batch * p->num_q_heads, G);
+  if (s != L4_OK) return s;
   char* ws = static_cast<char*>(workspace);
   RunArgs a;
   memset(&a, 0, sizeof(a));
@@ -1719,21 +1778,21 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   a.B = p->batch;
   a.forced_chunk = p->chunk_pages;
   a.items_cap = L.items_cap;
-  a.quad_bin = G <= kQuadMaxG ? kQuadBin : 0;
+  a.quad_bin = kQuadBin;
   a.early = fused && (p->flags & L4_DECODE_EARLY_INPUTS) != 0;
   if (fused) {
     switch (G) {
-      case 1: return launch_decode<1, true>(tk, tv, a, ctas, st);
-      case 2: return launch_decode<2, true>(tk, tv, a, ctas, st);
-      case 4: return launch_decode<4, true>(tk, tv, a, ctas, st);
-      default: return launch_decode<8, true>(tk, tv, a, ctas, st);
+      case 1: return launch_decode<1, true>(tk, tv, tq, a, ctas, st);
+      case 2: return launch_decode<2, true>(tk, tv, tq, a, ctas, st);
+      case 4: return launch_decode<4, true>(tk, tv, tq, a, ctas, st);
+      default: return launch_decode<8, true>(tk, tv, tq, a, ctas, st);
     }
   }
   switch (G) {
-    case 1: return launch_decode<1, false>(tk, tv, a, ctas, st);
-    case 2: return launch_decode<2, false>(tk, tv, a, ctas, st);
-    case 4: return launch_decode<4, false>(tk, tv, a, ctas, st);
-    default: return launch_decode<8, false>(tk, tv, a, ctas, st);
+    case 1: return launch_decode<1, false>(tk, tv, tq, a, ctas, st);
+    case 2: return launch_decode<2, false>(tk, tv, tq, a, ctas, st);
+    case 4: return launch_decode<4, false>(tk, tv, tq, a, ctas, st);
+    default: return launch_decode<8, false>(tk, tv, tq, a, ctas, st);
   }
 }
 

@@ -25,7 +25,8 @@ def timeit(fn, iters=40, warm=5):
 
 
 def main():
-    shape = bench.WORKLOADS["c2"]["shape"]
+    import synth
+    shape = synth.SHAPE_LLAMA3_70B if os.environ.get("SB_SHAPE") == "70b" else bench.WORKLOADS["c2"]["shape"]
     B = int(os.environ.get("SB_BATCH", "1024"))
     lengths = [int(x) for x in os.environ.get("SB_LENS", "64,128,176,192,200,208,240,256,320,512,530,1024").split(",")]
     for L in lengths:

@@ -32,24 +32,26 @@ for G, Hkv, chunk in ((4, 2, 0), (8, 1, 2), (1, 3, -1)):
     l4.decode_run(pe, qd, kd, vd, ix, o2, l2, ws)
     torch.cuda.synchronize()
     assert torch.equal(o2, out)
-# quad units: 1024 short requests x 8 kv heads (>= 4 quads per CTA), a few long ones ahead
-lens = np.random.default_rng(2).integers(1, 300, size=1024)
-lens[:3] = [5000, 0, 1]
-shape = synth.AttnShape("s", 32, 8)
-t = synth.make_page_table(lens, seed=2, spare_pages=3)
-q, k, v = synth.make_qkv_cpu(shape, t, seed=2)
-qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
-ip, ix, kl = (torch.from_numpy(x).cuda() for x in (t.indptr, t.indices, t.kv_len))
-pe = l4.make_params(len(lens), 32, 8, flags=l4.L4_DECODE_EARLY_INPUTS)
-ws = l4.alloc_workspace(pe, t.total_pages)
-o1, l1 = torch.empty(len(lens), 32, 128, device="cuda"), torch.empty(len(lens), 32, device="cuda")
-o2, l2 = torch.empty_like(o1), torch.empty_like(l1)
-for _ in range(2):
-    l4.attention_call(pe, qd, kd, vd, ip, ix, kl, t.total_pages, o1, l1, ws)
-l4.decode_plan(pe, kl, ip, t.total_pages, ws)
-l4.decode_run(pe, qd, kd, vd, ix, o2, l2, ws)
-torch.cuda.synchronize()
-assert torch.equal(o1, o2) and torch.isfinite(o1).all()
+# quad units: 1024 short requests x 8 kv heads (>= 4 quads per CTA), a few long ones ahead;
+# G = 4 (Q rows in the unit slot) and G = 8 (Q rows through the page ring)
+for Hq in (32, 64):
+    lens = np.random.default_rng(2).integers(1, 300, size=1024)
+    lens[:3] = [5000, 0, 1]
+    shape = synth.AttnShape("s", Hq, 8)
+    t = synth.make_page_table(lens, seed=2, spare_pages=3)
+    q, k, v = synth.make_qkv_cpu(shape, t, seed=2)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    ip, ix, kl = (torch.from_numpy(x).cuda() for x in (t.indptr, t.indices, t.kv_len))
+    pe = l4.make_params(len(lens), Hq, 8, flags=l4.L4_DECODE_EARLY_INPUTS)
+    ws = l4.alloc_workspace(pe, t.total_pages)
+    o1, l1 = torch.empty(len(lens), Hq, 128, device="cuda"), torch.empty(len(lens), Hq, device="cuda")
+    o2, l2 = torch.empty_like(o1), torch.empty_like(l1)
+    for _ in range(2):
+        l4.attention_call(pe, qd, kd, vd, ip, ix, kl, t.total_pages, o1, l1, ws)
+    l4.decode_plan(pe, kl, ip, t.total_pages, ws)
+    l4.decode_run(pe, qd, kd, vd, ix, o2, l2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.isfinite(o1).all()
 kk = torch.randn(2, 40, 2, 16, 128, device="cuda").to(torch.bfloat16)
 vv = torch.randn_like(kk)
 dk, dv = torch.zeros_like(kk), torch.zeros_like(vv)

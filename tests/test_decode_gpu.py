@@ -284,7 +284,7 @@ def test_fused_equals_plan_plus_run_bitwise(G, chunk):
     _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
 
 
-@pytest.mark.parametrize("G", [1, 2, 4])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_quad_units_short_batch(G):
     """Large batches of short requests run as quad units (four unsplit items per CTA unit, one
     per consumer warp, no merge), with the long requests CTA-wide before them and a CTA-wide
