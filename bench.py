@@ -419,13 +419,14 @@ def heterogeneity_slowdown(steps: int, warmup: int):
 
 def short_batches(steps: int, warmup: int):
     """Homogeneous batches of short requests at the largest single-launch batch (B = 1024,
-    Llama-3-8B shape): the per-item overheads the quad units remove."""
+    Llama-3-8B and -70B shapes): the per-item overheads the quad units remove."""
     import torch
     out = []
-    for L in (64, 200, 530):
-        w = Workload(f"short{L}", np.full(1024, L, dtype=np.int64), synth.SHAPE_LLAMA3_8B)
+    for shape, L in ((synth.SHAPE_LLAMA3_8B, 64), (synth.SHAPE_LLAMA3_8B, 200), (synth.SHAPE_LLAMA3_8B, 530),
+                     (synth.SHAPE_LLAMA3_70B, 64), (synth.SHAPE_LLAMA3_70B, 200)):
+        w = Workload(f"short{L}", np.full(1024, L, dtype=np.int64), shape)
         t, _, _ = time_steps(w, steps, warmup)
-        out.append(dict(length=L, batch=1024, us=round(t / steps * 1e3, 2),
+        out.append(dict(shape=shape.name, length=L, batch=1024, us=round(t / steps * 1e3, 2),
                         gbs=round(w.bytes_kv / (t / steps / 1e3) / 1e9, 1)))
         del w
         torch.cuda.empty_cache()
