@@ -55,6 +55,23 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def read_ceiling():
+    """HBM read ceiling measured on this pool by the development probe (scripts/readbw.py:
+    128-bit loads and TMA bulk reads of 1-4 GB, committed as profiles/readbw_r*.json), for
+    context: the decode kernel only reads, the roofline peak stays MEASURED_PEAKS.json's copy."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "readbw_r*.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+        except ValueError:
+            continue
+        vals = [v for k, v in d.items() if not k.startswith("copy") and isinstance(v, (int, float))]
+        if vals:
+            return float(max(vals)), os.path.relpath(f, ROOT)
+    return None, None
+
+
 def measured_traffic(workload: str):
     """dram__bytes_read.sum + dram__bytes_write.sum of one decode_kernel launch from the
     committed ncu --set full capture (profiles/*_traffic.json), or None."""
@@ -837,6 +854,7 @@ def main():
         extra["short_batches"] = short_batches(max(5, args.steps // 2), 3)
         extra["migration"] = migration_bandwidth()
         extra["partition_m6"] = partition_speed()
+    rceil, rceil_src = read_ceiling()
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(args.workload, budget_s=12.0)
@@ -874,7 +892,10 @@ def main():
                      "traffic_source": traffic_src,
                      "peak_source": peak_src, "launch_ms": round(launch_avg, 5),
                      "bytes_per_launch": wl.bytes_algo,
-                     "frac_of_nominal_8TBs": round(achieved / 8000.0, 4)},
+                     "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
+                     "read_ceiling_gbs": rceil,
+                     "frac_of_read_ceiling": round(achieved / rceil, 4) if rceil else None,
+                     "read_ceiling_source": rceil_src},
         "isolated_call": {"note": "l4_decode_attention without L4_DECODE_EARLY_INPUTS: each call starts "
                                   "reading after the previous one completed",
                           "ms_per_step": round(iso_ms / args.steps, 5),

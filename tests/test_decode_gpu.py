@@ -284,32 +284,34 @@ def test_fused_equals_plan_plus_run_bitwise(G, chunk):
     _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
 
 
-@pytest.mark.parametrize("G", [1, 2, 4, 8])
-def test_quad_units_short_batch(G):
+@pytest.mark.parametrize("G,chunk", [(1, 0), (2, 0), (4, 0), (8, 0), (4, -1), (4, 3), (8, 6)])
+def test_quad_units_short_batch(G, chunk):
     """Large batches of short requests run as quad units (four unsplit items per CTA unit, one
     per consumer warp, no merge), with the long requests CTA-wide before them and a CTA-wide
     tail after them.  8192 items (B = 1024, 8 kv heads) clear the >= 4 quads per CTA threshold.
     Ragged lengths (NaN-poisoned tails), empty requests, items of 32..63 pages (the second
     block of page ids), fp32 and bf16 outputs; fused == plan + run bitwise; early-input
-    back-to-back calls bitwise; oracle within 2e-3."""
+    back-to-back calls bitwise; oracle within 2e-3.  Forced chunks: -1 (no splits: every item
+    of <= 63 pages is quad-eligible), 3 and 6 (quad bins shrink to items of <= 2C/3 pages, the
+    split requests' pieces run CTA-wide)."""
     rng = np.random.default_rng(300 + G)
     lens = rng.integers(1, 1009, size=1024)
     lens[:6] = [0, 1, 16, 1008, 513, 0]
     lens[-3:] = [9000, 20000, 3000]  # CTA-wide items ahead of the quad suffix
     Hkv = 8
     table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, Hkv * G, Hkv, seed=G)
-    params = l4.make_params(table.batch, Hkv * G, Hkv)
+    params = l4.make_params(table.batch, Hkv * G, Hkv, chunk_pages=chunk)
     ws = l4.alloc_workspace(params, table.total_pages)
     o1, l1 = _plan_run(params, table, qd, kd, vd, ip, ix, kl, ws)
     o2, l2 = _fused(params, table, qd, kd, vd, ip, ix, kl, ws)
-    pe = l4.make_params(table.batch, Hkv * G, Hkv, flags=l4.L4_DECODE_EARLY_INPUTS)
+    pe = l4.make_params(table.batch, Hkv * G, Hkv, chunk_pages=chunk, flags=l4.L4_DECODE_EARLY_INPUTS)
     early = [_fused(pe, table, qd, kd, vd, ip, ix, kl, ws) for _ in range(3)]
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
     for o4, l4_ in early:
         assert torch.equal(o2, o4) and torch.equal(l2, l4_)
     _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
-    pb = l4.make_params(table.batch, Hkv * G, Hkv, out_dtype=l4.L4_DT_BF16)
+    pb = l4.make_params(table.batch, Hkv * G, Hkv, out_dtype=l4.L4_DT_BF16, chunk_pages=chunk)
     ob = torch.empty(table.batch, Hkv * G, 128, device="cuda", dtype=torch.bfloat16)
     lb = torch.empty(table.batch, Hkv * G, device="cuda")
     l4.attention_call(pb, qd, kd, vd, ip, ix, kl, table.total_pages, ob, lb, ws)
