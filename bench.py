@@ -679,7 +679,8 @@ def pipeline_line(args, world, rank, local):
             clk = clocks.stop()
         vec = torch.tensor([t["kv_bytes"], t["tokens"], t["mig_bytes"], t["mig_count"], t["req_steps"],
                             t["lat_ms_x_req"], t["launches"], t["precopy_pages"], t["stop_pages"],
-                            t["single_pages"], t.get("h2d", 0), t.get("d2h", 0)], dtype=torch.float64, device=cdev)
+                            t["single_pages"], t.get("h2d", 0), t.get("d2h", 0), t["busy_ms"]],
+                           dtype=torch.float64, device=cdev)
         dist.all_reduce(vec, op=dist.ReduceOp.SUM)
         tm = torch.tensor([t["elapsed_ms"], t["busy_ms"]], dtype=torch.float64, device=cdev)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -694,6 +695,7 @@ def pipeline_line(args, world, rank, local):
                          stage_cv=[round(x, 4) for x in t["stage_cv"]],
                          launches=int(vec[6]), precopy_pages=int(vec[7]), stop_round_pages=int(vec[8]),
                          single_round_pages=int(vec[9]), h2d_bytes=int(vec[10]), d2h_bytes=int(vec[11]),
+                         sum_busy_ms=float(vec[12]), kv_bytes=float(vec[0]),
                          stages=[list(x) for x in st])
     if rank != 0:
         return None
@@ -720,6 +722,13 @@ def pipeline_line(args, world, rank, local):
         "gpu_launches": int(l4r["launches"]),
         "clocks": clk,
     }
+    # dominant kernel: the per-step decode launch of every rank (algorithmic KV bytes over the
+    # summed event time of those launches, all ranks)
+    ach = l4r["kv_bytes"] / (l4r["sum_busy_ms"] / 1e3) / 1e9 if l4r["sum_busy_ms"] > 0 else None
+    line["roofline"] = {"bound": "hbm", "kernel": "decode_kernel<G, fused> (per-rank l4_decode_attention)",
+                        "achieved": round(ach, 1) if ach else None, "peak": peak, "unit": "GB/s",
+                        "frac": round(ach / peak, 4) if ach else None, "traffic": None, "peak_source": peak_src,
+                        "note": "KV bytes only (q/out/ids not counted); per-GPU"}
     e = res["l4_e2e"]
     line["e2e"] = {"value": round(e["kv_gbs"], 1), "unit": "GB/s",
                    "h2d_bytes_per_step": int(e["h2d_bytes"] / max(1, args.steps)),
