@@ -1752,9 +1752,13 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   if (s != L4_OK) return s;
   s = make_tmap(&tv, v_pages, rows);
   if (s != L4_OK) return s;
-  CUtensorMap tq;  // q [B * Hq rows of 256 B]: one box = the G query rows of a kv group (2-D TMA)
-  s = make_qmap(&tq, q, (int64_t)p->batch * p->num_q_heads, G);
-  if (s != L4_OK) return s;
+  // q [B * Hq rows of 256 B]: one box = the G query rows of a kv group (2-D TMA); read only by
+  // the G = 8 quad units (ring_q), so the other group sizes skip the host-side encode
+  CUtensorMap tq = tk;
+  if (G > kQuadMaxG && kQuadBin > 0) {
+    s = make_qmap(&tq, q, (int64_t)p->batch * p->num_q_heads, G);
+    if (s != L4_OK) return s;
+  }
   char* ws = static_cast<char*>(workspace);
   RunArgs a;
   memset(&a, 0, sizeof(a));
