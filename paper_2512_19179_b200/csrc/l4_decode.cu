@@ -605,10 +605,7 @@ struct SmemLayout {
   static constexpr int nbars = 2 * stages_n + 2 * kItemSlots;
   static constexpr int seq = bars + nbars * 8;  // int [stages_n]: page sequence number armed per stage
   static constexpr int flag = seq + stages_n * 4;
-#ifndef L4_SMEM_PAD
-#define L4_SMEM_PAD 0
-#endif
-  static constexpr int total = align16c(flag + 16) + (G <= 4 ? L4_SMEM_PAD : 0);  // pad: development experiments only
+  static constexpr int total = align16c(flag + 16);
   static constexpr int alloc = total + 1024;  // room to align the base to 1024 B (128B swizzle)
   static_assert(merge_o % 16 == 0 && total % 16 == 0 && bars % 8 == 0, "aligned areas");
 };
