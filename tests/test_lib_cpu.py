@@ -281,3 +281,18 @@ def test_qoe_fit_matches_lstsq_oracle():
     with pytest.raises(l4.L4Error) as e:
         l4.qoe_fit(G, np.ones(10))
     assert e.value.status == l4.L4_ERR_INFEASIBLE
+
+
+def test_quad_bin_bound_holds_for_every_chunk():
+    """Host-side check of the decode planner's quad-bin bound: with chunk C, a
+    request of p > 2C pages is split into ceil(p / C) near-equal pieces whose largest has more
+    than 2C/3 pages, so bins b with 2^b - 1 <= floor(2C/3), i.e. b <= bit_length(floor(2C/3) + 1)
+    - 1 (capped at 6), contain unsplit requests only.  Exhaustive over C <= 600, p <= 8C."""
+    for C in range(1, 601):
+        qb = min(6, ((2 * C) // 3 + 1).bit_length() - 1)
+        assert (1 << qb) - 1 <= (2 * C) // 3
+        for p in range(2 * C + 1, 8 * C + 1):
+            ns = -(-p // C)
+            largest = -(-p // ns)
+            assert 3 * largest > 2 * C
+            assert largest.bit_length() > qb  # a split request never lands in a quad bin
