@@ -321,6 +321,19 @@ def test_quad_units_short_batch(G, chunk):
     assert torch.equal(lb, l2)
 
 
+@pytest.mark.parametrize("Hq", [32, 64])
+def test_quad_units_materialised_plan(Hq):
+    """B > 1024 takes the materialised plan (planner kernel + run kernel): quad units there too,
+    for G = 4 (Q rows in the unit slot) and G = 8 (Q rows through the page ring), vs the oracle."""
+    rng = np.random.default_rng(77 + Hq)
+    lens = rng.integers(0, 300, size=2048)
+    lens[:2] = [4000, 1]
+    table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, Hq, 8, seed=Hq)
+    out, lse = l4.decode_attention(qd, kd, vd, ip, ix, kl)
+    torch.cuda.synchronize()
+    _check(out.double().cpu().numpy(), lse.double().cpu().numpy(), ro, rl)
+
+
 def test_fused_workspace_reuse_across_batch_sizes():
     """One workspace, calls with different B (and split-heavy plans) back to back: the split
     counters live in a region independent of B, so no call sees another call's stale items."""
