@@ -1451,8 +1451,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     // here but resolved at the end of this CTA's NEXT item, so no consumer waits for an atomic
     // round trip between items.  Counters are self-cleaning (reset by the last arrival).
     // Release: bar.sync orders every thread's partial stores before thread 0's acq_rel ticket
-    // (cumulative); acquire: the ticket, then bar.sync, then ld.global.cg reads.
-    named_bar_sync(1, kConsumerThreads);
+    // (cumulative); acquire: the ticket, then bar.sync, then ld.global.cg reads.  An unsplit item
+    // with no pending ticket needs only the final barrier (merge area free).
+    if (split || has_pend) named_bar_sync(1, kConsumerThreads);
     if (has_pend && ct == 0) {
       const int last = (pend_old == group_need(pend_it) - 1);
       if (last) *group_ctr(pend_it) = 0;
