@@ -556,7 +556,7 @@ struct RunArgs {
   const int* kv_len;
   const int* indptr;
   int B, forced_chunk, items_cap;
-  int quad_bin;  // kQuadBin for G <= 4, else 0 (no quad units)
+  int quad_bin;  // kQuadBin (0: no quad units)
   int early;  // L4_DECODE_EARLY_INPUTS: read inputs before griddepcontrol.wait (fused path)
 };
 
@@ -1006,9 +1006,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       if constexpr (kStages % kConsumerWarps != 0) st_release_cta(sbase + SL::seq + st * 4, (int)qseq);
       mbar_arrive(bar_full + st * 8);
     };
-    // Quad unit u (items f .. f + nsub - 1, one per consumer warp): lane w < nsub posts item w
-    // and its Q rows; page j of item w goes out as ring page qbase + 4 j + w (null stages pad
-    // the shorter items), so warp w always owns the ring pages = w (mod 4) of the unit.
+    // Quad unit u (items f .. f + 3, one per consumer warp): lanes 0..3 look up one item each,
+    // lane 0 posts the slot and issues the Q rows (slot copies, or ring positions qbase + w at
+    // G = 8); page j of item w goes out as ring page qbase' + 4 j + w (null stages pad the
+    // shorter items), so warp w always owns the ring positions = w (mod 4) of the unit.
     auto issue_quad = [&](int u, uint32_t kk) {
       if constexpr (SL::quads) {
         const int f = unit_item(u);
