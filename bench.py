@@ -914,6 +914,10 @@ def main():
                    "call": "l4_decode_attention (plan + split-KV + combine in one kernel launch), "
                            "flags=L4_DECODE_EARLY_INPUTS, back-to-back steps"},
         "tokens_per_s": round(ws * len(wl.lens) / (ms_step / 1e3), 1),
+        "tokens_per_s_depth_normalised": {
+            "value": round(ws * len(wl.lens) / (ms_step / 1e3) / (80 if wl.shape.num_q_heads == 64 else 32), 1),
+            "layers": 80 if wl.shape.num_q_heads == 64 else 32,
+            "note": "SURVEY 8(d): B / (n_layers x t_call), attention time only (Llama-3-8B 32 / -70B 80 layers)"},
         "pct_hbm_peak": round(100.0 * value / (ws * peak), 2),
         "roofline": {"bound": "hbm", "kernel": "decode_kernel<G, fused> (l4_decode_attention, "
                                                "L4_DECODE_EARLY_INPUTS)",
