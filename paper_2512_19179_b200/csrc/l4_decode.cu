@@ -131,7 +131,7 @@ __device__ __forceinline__ unsigned long long trace_now() {
 struct __align__(16) PlanHeader {
   int n_items, chunk, num_ctas, max_splits;
   int batch, num_kv_heads, items_cap, n_wide;  // n_wide: items before the quad units
-  int tail_requests, tail_chunk, pad2[6];
+  int tail_requests, tail_chunk, quad_pages, pad2[5];  // quad_pages: see plan_core's QPages_out
   int sched_next, sched_done, pad3[14];  // ticket counter and finished-CTA count (self-resetting)
 };
 static_assert(sizeof(PlanHeader) == 128, "PlanHeader is 128 bytes");
@@ -281,7 +281,7 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
 }
 
 // Shared-memory scratch of plan_core (bytes; 8-byte aligned base).
-constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4;
+constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4 + 32 * 4;
 
 // The planner (a1), run by every thread of a CTA: reads kv_len / indptr, chooses the chunk C,
 // and orders the requests by length bin, longest bin first, request index ascending inside a
@@ -295,12 +295,13 @@ constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWa
 __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict__ indptr, int B, int Hkv,
                           int num_ctas, int forced_chunk, int items_cap, int* s_len, int* s_ptr, int* s_rb,
                           int* s_off, unsigned char* scratch, int* C_out, int* N_out, int* Pmax_out,
-                          int quad_bin, int* Wide_out) {
+                          int quad_bin, int* Wide_out, int* QPages_out) {
   long long* s_ll = reinterpret_cast<long long*>(scratch);
   int* s_i = reinterpret_cast<int*>(scratch + 32 * 8);
   unsigned* s_u = reinterpret_cast<unsigned*>(scratch + 32 * 8 + 36 * 4);
   int* s_w = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4);        // per-warp sums
   int* s_wcnt = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4);  // [nw][kNumBins]
+  int* s_ms = s_wcnt + kPlanMaxWarps * kNumBins;  // per-warp lowest bin of a split request
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nw = nthr >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -341,8 +342,9 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   const int tpw = (tiles + nw - 1) / nw;
   const int r0 = min(B, warp * tpw * 32), r1 = min(B, r0 + tpw * 32);
   long long N;
+  int min_split_bin;
   for (;;) {
-    int wsum = 0;
+    int wsum = 0, wms = kNumBins;
     for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 1: per-warp bin histogram + item count
       const int b = t0 + lane;
       int bin = -1;
@@ -351,17 +353,28 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
         const int ns = nsplit_of(pg, C);
         bin = bin_of(pg, ns);
         wsum += ns;
+        if (ns > 1) wms = min(wms, bin);
       }
       const unsigned peers = __match_any_sync(0xffffffffu, bin);
       if (bin >= 0 && (peers & lt_mask) == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
       __syncwarp();
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-    if (lane == 0) s_w[warp] = wsum;  // not s_i: slower warps may still read block_reduce3's s_i
+    for (int o = 16; o; o >>= 1) {
+      wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+      wms = min(wms, __shfl_xor_sync(0xffffffffu, wms, o));
+    }
+    if (lane == 0) {
+      s_w[warp] = wsum;  // not s_i: slower warps may still read block_reduce3's s_i
+      s_ms[warp] = wms;
+    }
     __syncthreads();
     N = 0;
-    for (int w = 0; w < nw; ++w) N += s_w[w];
+    min_split_bin = kNumBins;
+    for (int w = 0; w < nw; ++w) {
+      N += s_w[w];
+      min_split_bin = min(min_split_bin, s_ms[w]);
+    }
     N *= Hkv;
     if (N <= items_cap || C >= INT_MAX / 8) break;
     C *= 2;
@@ -369,10 +382,10 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     __syncthreads();
   }
   if (tid == 0) L4_MARK(7);
-  // Quad bins: every item of bins <= quad_bin must be unsplit.  A split request (> 2C pages,
-  // ceil(pages / C) splits) has a largest split of more than 2C/3 pages, so bins whose items have
-  // at most 2C/3 pages (2^bin - 1 <= floor(2C/3)) hold unsplit requests only.
-  if (quad_bin > 0) quad_bin = min(quad_bin, 31 - __clz((2 * C) / 3 + 1));
+  // Quad bins: every item of bins <= quad_bin must be unsplit, so the quad bins end below the
+  // lowest bin that holds a split request (a split request's largest split has more than 2C/3
+  // pages, so this never cuts below bit_length(floor(2C/3) + 1) - 1).
+  if (quad_bin > 0) quad_bin = min(quad_bin, min_split_bin - 1);
   if (warp == 0) {  // bases: bins in descending order, then warps in request order
     const int bin = kNumBins - 1 - lane;
     int tot = 0;
@@ -450,7 +463,10 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   *N_out = (int)N;
   *Pmax_out = Pmax;
   // items before the first quad-bin rank run CTA-wide; the rest are grouped four per unit
-  *Wide_out = (quad_bin > 0 && quad_rank < B) ? s_off[quad_rank] : (int)N;
+  const bool has_quads = quad_bin > 0 && quad_rank < B;
+  *Wide_out = has_quads ? s_off[quad_rank] : (int)N;
+  // pages of the first quad-eligible request (its bin is the largest; within a bin, < 2x more)
+  *QPages_out = has_quads ? pages_of(s_len[s_rb[quad_rank] & 0xffff]) : 0;
 }
 
 // Work item `i` of the plan held in shared memory (fused path) — the same item plan_kernel
@@ -498,9 +514,9 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
   int* s_rb = s_ptr + Bs;
   int* s_off = s_rb + Bs;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  int C, N, Pmax, Nw;
+  int C, N, Pmax, Nw, Qb;
   plan_core(a.kv_len, a.indptr, a.B, a.Hkv, a.num_ctas, a.forced_chunk, a.items_cap, s_len, s_ptr, s_rb, s_off,
-            scratch, &C, &N, &Pmax, a.quad_bin, &Nw);
+            scratch, &C, &N, &Pmax, a.quad_bin, &Nw, &Qb);
   // ---- items: one thread per (request rank, kv head) writes that pair's splits
   for (int x = tid; x < a.B * a.Hkv; x += nthr) {
     const int r = x / a.Hkv, h = x - r * a.Hkv;
@@ -531,6 +547,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     hd.num_kv_heads = a.Hkv;
     hd.items_cap = a.items_cap;
     hd.n_wide = Nw;
+    hd.quad_pages = Qb;
     hd.sched_next = 0;
     hd.sched_done = 0;
     *a.header = hd;
@@ -902,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     raw_t1 = atomicAdd(&a.header->sched_next, 1);
     raw_t2 = atomicAdd(&a.header->sched_next, 1);
   }
-  int n_items, plan_C = 0, n_wide;
+  int n_items, plan_C = 0, n_wide, q_pages = 0;
   int *p_len = nullptr, *p_ptr = nullptr, *p_rb = nullptr, *p_off = nullptr;
   if constexpr (kFused) {
     // a1 in every CTA: the plan lives in this CTA's shared memory (scratch in the merge area,
@@ -913,10 +930,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     p_off = p_rb + a.B;
     int pmax;
     plan_core(a.kv_len, a.indptr, a.B, a.Hkv, W, a.forced_chunk, a.items_cap, p_len, p_ptr, p_rb, p_off,
-              smem + SL::merge_o, &plan_C, &n_items, &pmax, SL::quads ? a.quad_bin : 0, &n_wide);
+              smem + SL::merge_o, &plan_C, &n_items, &pmax, SL::quads ? a.quad_bin : 0, &n_wide, &q_pages);
   } else {
     n_items = a.header->n_items;
     n_wide = SL::quads ? a.header->n_wide : n_items;
+    q_pages = a.header->quad_pages;
   }
   // Scheduling units: items [0, n_wide) one per unit (CTA-wide); then the quad-eligible suffix
   // four items per unit (one per consumer warp), except its last kQuadTailPerCta x W items,
@@ -925,7 +943,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   // warp alone streams a page at a fraction of a CTA's share of HBM bandwidth).
   const int q_rest = n_items - n_wide;
   int n_quads = (q_rest - min(q_rest, kQuadTailPerCta * W)) / kQuad;
-  if (n_quads < kQuadMinPerCta * W) n_quads = 0;
+  // A quad is the launch's granularity at the end: units of at most ~16 pages need one per CTA,
+  // larger ones up to kQuadMinPerCta per CTA (q_pages = pages of the largest quad item)
+  if (n_quads < min(kQuadMinPerCta, max(1, (q_pages + 3) / 4)) * W) n_quads = 0;
   const int n_units = n_items - (kQuad - 1) * n_quads;
   const int u_tail = n_wide + n_quads;  // first tail unit
   if (threadIdx.x == 0) L4_MARK(2);
