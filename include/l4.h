@@ -114,6 +114,24 @@ size_t l4_decode_workspace_size(const l4_decode_params* p, int64_t max_total_pag
 l4_status l4_decode_workspace_init(const l4_decode_params* p, void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/* Byte regions of a workspace of `workspace_bytes` (host-only, no device access; diagnostics
+ * and tests).  [0, state_bytes) holds the scheduler header and the split counters (must be
+ * zero between calls); [partial_lse_offset, +items_cap*G*4) the base-2 LSE of the split
+ * partials and [partial_o_offset, +items_cap*G*128*4) their normalised outputs (fp32), both
+ * indexed by work item.  Nothing in the partial regions survives a call as state: a test may
+ * fill them with NaN before every call so that a combine reading a partial before it was
+ * written shows up as NaN.  Errors: INVALID_ARG (params), WORKSPACE (too small). */
+typedef struct {
+  uint64_t state_bytes;
+  uint64_t partial_lse_offset;
+  uint64_t partial_o_offset;
+  uint64_t end_offset;          /* end of the partial region (<= workspace_bytes) */
+  int32_t  items_cap;           /* work-item / partial-slot capacity */
+  int32_t  group_size;          /* G = Hq / Hkv */
+} l4_workspace_regions;
+l4_status l4_decode_workspace_regions(const l4_decode_params* p, size_t workspace_bytes,
+                                      l4_workspace_regions* out);
+
 /* a1: build the length-binned work list for this step from device kv_len [B]
  * and page_indptr [B+1] into `workspace` (one device kernel, graph-capturable,
  * no host synchronisation).  The plan stays valid for any number of
@@ -274,7 +292,11 @@ typedef struct {
  * page's K and V slices of every layer straight into the destination slots
  * (no staging buffer).  If done_event (cudaEvent_t) is non-NULL it is
  * recorded after the copy.  The caller frees the source pages only after the
- * copy completed (exactly-once ownership).  src_pages: host int32 [n]. */
+ * copy completed (exactly-once ownership).  src_pages: host int32 [n].
+ * Errors after the allocation: a failed launch returns L4_ERR_CUDA with the destination pages
+ * back in the pool once the copies already enqueued have drained (if that synchronisation also
+ * fails they stay allocated and their ids are in dst_pages_out); a failed cudaEventRecord returns
+ * L4_ERR_CUDA with the copy enqueued and the allocated ids in dst_pages_out. */
 l4_status l4_migrate(const l4_kv_view* src, const int32_t* src_pages, int64_t n_pages, const l4_kv_view* dst,
                      l4_page_pool* dst_pool, int32_t* dst_pages_out, void* stream, void* done_event);
 

@@ -42,6 +42,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -125,6 +126,20 @@ __device__ __forceinline__ unsigned long long trace_now() {
 #define L4_TRACE_FLUSH(k) (g_trace[blockIdx.x * 16 + (k)] = tr_acc[(k)])
 #else
 #define L4_MARK(k) ((void)0)
+#endif
+
+#ifdef L4_DEBUG_CKS
+// Development-only data checksums per work item (scripts/flake_split.py --cks): XOR of the K and
+// V fragments the consumers loaded, XOR of the Q fragments, weighted sum of the page ids the
+// producer issued, built only into debug variants (-DL4_DEBUG_CKS).
+__device__ unsigned g_cks[16384 * 4];
+#endif
+#ifdef L4_DEBUG_PAGE
+// Development-only per-(page, kv head) record of one call: K / V fragment checksums and where the
+// slice was consumed (CTA, ring sequence number, page index in its item | warp << 16, item).
+constexpr int kDbgPages = 1 << 21;
+__device__ unsigned g_pk[kDbgPages], g_pv[kDbgPages];
+__device__ uint4 g_pmeta[kDbgPages];
 #endif
 
 // Header region (256 B): plan summary + dynamic scheduler state.
@@ -772,7 +787,7 @@ __device__ __forceinline__ uint32_t slice_off(int t, int cd) {
 // One page (16 tokens) of one (request, kv head): S^T = K Q^T, online softmax, O^T += V^T P^T.
 __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const uint32_t (&qf)[8][2],
                                              float (&acc)[8][4], float (&mrow)[2], float (&lrow)[2],
-                                             float scale_log2, int lane) {
+                                             float scale_log2, int lane, uint32_t& cks_k, uint32_t& cks_v) {
   using namespace dev;
   const int g = lane >> 2, c = lane & 3;
   const int mi = lane >> 3, r8 = lane & 7;
@@ -785,9 +800,20 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
     for (int kk = 0; kk < 8; ++kk) {
       uint32_t a0, a1, a2, a3;
       ldmatrix_x4(sbase + slice_off(tok, kk * 2 + (mi >> 1)), a0, a1, a2, a3);
+      cks_k ^= a0 ^ a1 ^ a2 ^ a3;  // debug checksum (dead code unless L4_DEBUG_CKS)
       mma_bf16_16816(s, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
     }
   }
+#ifdef L4_DEBUG_VEARLY
+  uint32_t vf[8][4];  // experiment: every V fragment read before the softmax
+  {
+    const int tok = r8 + ((mi >> 1) << 3);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+      ldmatrix_x4_trans(sbase + kSliceBytes + slice_off(tok, mt * 2 + (mi & 1)), vf[mt][0], vf[mt][1], vf[mt][2],
+                        vf[mt][3]);
+  }
+#endif
   // ---- mask (Z20: tokens >= kv_len are not attended) and online softmax in the exp2 domain
   const float NEG = -INFINITY;
   const float t0 = (g < valid) ? s[0] * scale_log2 : NEG;
@@ -831,13 +857,19 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
       uint32_t a0, a1, a2, a3;
+#ifdef L4_DEBUG_VEARLY
+      a0 = vf[mt][0]; a1 = vf[mt][1]; a2 = vf[mt][2]; a3 = vf[mt][3];
+      (void)vbase; (void)tok;
+#else
       ldmatrix_x4_trans(vbase + slice_off(tok, mt * 2 + (mi & 1)), a0, a1, a2, a3);
+#endif
       if (valid < kPage) {
         a0 &= mlo;
         a1 &= mlo;
         a2 &= mhi;
         a3 &= mhi;
       }
+      cks_v ^= a0 ^ a1 ^ a2 ^ a3;
       mma_bf16_16816(acc[mt], a0, a1, a2, a3, bh0, bh1);
       mma_bf16_16816(acc[mt], a0, a1, a2, a3, bl0, bl1);
     }
@@ -886,7 +918,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < kStages; ++i) s_seq[i] = -1;
     for (int i = 0; i < kStages; ++i) {
       mbar_init(bar_full + i * 8, 1);
+#ifdef L4_DEBUG_ALLARRIVE
+      mbar_init(bar_empty + i * 8, 32);  // experiment: every lane of the consuming warp arrives
+#else
       mbar_init(bar_empty + i * 8, 1);
+#endif
     }
     for (int i = 0; i < kItemSlots; ++i) {
       mbar_init(bar_ifull + i * 8, 1);
@@ -1134,6 +1170,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int j = 0; j < cnt; ++j) {
           const int page = __shfl_sync(0xffffffffu, blk, j);
           if (lane == 0) issue_page(page, cur.h);
+#ifdef L4_DEBUG_CKS
+          if (lane == 0 && unit_item(i_cur) < 16384)
+            atomicAdd(&g_cks[unit_item(i_cur) * 4 + 3], (unsigned)page * (unsigned)(j0 + j + 1));
+#endif
           ++qseq;
         }
         blk = nb;
@@ -1181,6 +1221,10 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int j = max(jstart - j0, 0); j < cnt; ++j) {
             const int page = __shfl_sync(0xffffffffu, blk, j);
             if (lane == 0) issue_page(page, cur.h);
+#ifdef L4_DEBUG_CKS
+            if (lane == 0 && unit_item(i_cur) < 16384)
+              atomicAdd(&g_cks[unit_item(i_cur) * 4 + 3], (unsigned)page * (unsigned)(j0 + j + 1));
+#endif
             ++qseq;
           }
           blk = nb;
@@ -1231,6 +1275,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     return a.counters + (size_t)w.b * a.Hkv + w.h;
   };
   auto finish_group = [&](const WorkItem& w) {  // this CTA was the last split of w's group
+#ifdef L4_DEBUG_FENCE
+    __threadfence();  // experiment: every reader fences before reading the partials
+#endif
     const int ns = w.nsplit;
     const int ng = (ns + kCombineGroup - 1) / kCombineGroup;
     const int g0 = (w.split / kCombineGroup) * kCombineGroup;
@@ -1304,6 +1351,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
       float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+      uint32_t cks_k = 0, cks_v = 0;
       const int np = mine ? it.pend - it.pbeg : 0;
       for (int j = 0; j < maxnp; ++j) {
         const uint32_t q = qbase + kQuad * j + warp;
@@ -1315,7 +1363,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(bar_full + st * 8, (q / kStages) & 1);
         if (j < np)
           consume_page(sbase + SL::stages + st * kStageBytes, (j == np - 1) ? it.last_valid : kPage, qf, acc, mrow,
-                       lrow, a.scale_log2, lane);
+                       lrow, a.scale_log2, lane, cks_k, cks_v);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty + st * 8);
       }
@@ -1370,6 +1418,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
     float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+    uint32_t cks_k = 0, cks_v = 0;
     const int np = it.pend - it.pbeg;
     for (int j = warp; j < np; j += kConsumerWarps) {
       const uint32_t q = qbase + j;
@@ -1382,6 +1431,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       mbar_wait(bar_full + st * 8, (q / kStages) & 1);
+#ifdef L4_DEBUG_RAW_FENCE
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment: after the wait, before reads
+#endif
 #ifdef L4_TRACE
       if (q == 0 && lane == 0) L4_MARK(4);
       if (warp == 0 && lane == 0) trace_add(12, trace_now() - tw0);
@@ -1390,15 +1442,59 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef L4_TRACE
       const unsigned long long tc0 = trace_now();
 #endif
-      consume_page(sbase + SL::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane);
+#ifdef L4_DEBUG_PAGE
+      const uint32_t ck0 = cks_k, cv0 = cks_v;
+#endif
+      consume_page(sbase + SL::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane, cks_k, cks_v);
+#ifdef L4_DEBUG_PAGE
+      {
+        uint32_t dk = cks_k ^ ck0, dv = cks_v ^ cv0;
+        for (int o = 16; o; o >>= 1) {
+          dk ^= __shfl_xor_sync(0xffffffffu, dk, o);
+          dv ^= __shfl_xor_sync(0xffffffffu, dv, o);
+        }
+        const int page = __ldg(a.indices + it.pbeg + j);
+        const long long key = (long long)page * a.Hkv + it.h;
+        if (lane == 0 && key < kDbgPages) {
+          g_pk[key] = dk;
+          g_pv[key] = dv;
+          g_pmeta[key] = make_uint4(blockIdx.x, q, (unsigned)j | ((unsigned)warp << 16) | ((unsigned)k << 20), item_idx);
+        }
+      }
+#endif
 #ifdef L4_TRACE
       if (warp == 0 && lane == 0) trace_add(11, trace_now() - tc0);
 #endif
       __syncwarp();
+#ifdef L4_DEBUG_PROXY_FENCE
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment: generic reads before TMA writes
+#endif
+#ifdef L4_DEBUG_ALLARRIVE
+      mbar_arrive(bar_empty + st * 8);
+#else
       if (lane == 0) mbar_arrive(bar_empty + st * 8);
+#endif
     }
     qbase += np;
     if (early && k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
+#ifdef L4_DEBUG_CKS
+    {
+      uint32_t cq = 0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) cq ^= qf[kk][0] ^ (qf[kk][1] * 3u);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        cks_k ^= __shfl_xor_sync(0xffffffffu, cks_k, o);
+        cks_v ^= __shfl_xor_sync(0xffffffffu, cks_v, o);
+        cq ^= __shfl_xor_sync(0xffffffffu, cq, o);
+      }
+      if (lane == 0 && item_idx < 16384) {
+        atomicXor(&g_cks[item_idx * 4 + 0], cks_k * (2u * warp + 1u));
+        atomicXor(&g_cks[item_idx * 4 + 1], cks_v * (2u * warp + 1u));
+        if (warp == 0) atomicXor(&g_cks[item_idx * 4 + 2], cq);
+      }
+    }
+#endif
 #ifdef L4_TRACE
     const unsigned long long te0 = trace_now();
 #endif
@@ -1474,6 +1570,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     // Release: bar.sync orders every thread's partial stores before thread 0's acq_rel ticket
     // (cumulative); acquire: the ticket, then bar.sync, then ld.global.cg reads.  An unsplit item
     // with no pending ticket needs only the final barrier (merge area free).
+#ifdef L4_DEBUG_FENCE
+    if (split) __threadfence();  // experiment: every thread fences its own partial stores
+#endif
     if (split || has_pend) named_bar_sync(1, kConsumerThreads);
     if (has_pend && ct == 0) {
       const int last = (pend_old == group_need(pend_it) - 1);
@@ -1574,11 +1673,11 @@ l4_status make_tmap(CUtensorMap* tm, const void* base, int64_t rows) {
 template <int G, bool kFused>
 l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tq, const RunArgs& a,
                         int grid, cudaStream_t st) {
-  static bool attr_set[64] = {false};
+  static std::atomic<bool> attr_set[64];  // per device; cudaFuncSetAttribute is idempotent
   const size_t smem_max = SmemLayout<G>::alloc + (kFused ? fused_plan_bytes(kFusedMaxBatch) : 0);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 64 && !attr_set[dev]) {
+  if (dev < 64 && !attr_set[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<G, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_max);
     if (e == cudaSuccess)
@@ -1589,7 +1688,7 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const CUte
       cudaGetLastError();
       return L4_ERR_CUDA;
     }
-    attr_set[dev] = true;
+    attr_set[dev].store(true, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1611,13 +1710,16 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const CUte
 }
 
 l4_status device_ctas(int* ctas_out) {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];  // per device (0 = not queried yet); racing first calls agree
   int dev = 0;
   l4_status s = get_device(&dev);
   if (s != L4_OK) return s;
-  if (dev < 64 && cache[dev] > 0) {
-    *ctas_out = cache[dev];
-    return L4_OK;
+  if (dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) {
+      *ctas_out = c;
+      return L4_OK;
+    }
   }
   int sms = 0;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1633,7 +1735,7 @@ l4_status device_ctas(int* ctas_out) {
     return L4_ERR_CUDA;
   }
   const int ctas = sms * 2;  // two persistent CTAs per SM (~92 KB shared memory, 160 threads each)
-  if (dev < 64) cache[dev] = ctas;
+  if (dev < 64) cache[dev].store(ctas, std::memory_order_relaxed);
   *ctas_out = ctas;
   return L4_OK;
 }
@@ -1656,6 +1758,24 @@ extern "C" size_t l4_decode_workspace_size(const l4_decode_params* p, int64_t ma
   return ws_layout(p->batch, p->num_kv_heads, G, cap).total;
 }
 
+#ifdef L4_DEBUG_CKS
+extern "C" int l4_debug_cks(unsigned* host, int n, int clear) {
+  if (clear) {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, g_cks);
+    return (int)cudaMemset(p, 0, sizeof(unsigned) * 16384 * 4);
+  }
+  return (int)cudaMemcpyFromSymbol(host, g_cks, sizeof(unsigned) * (size_t)n);
+}
+#endif
+#ifdef L4_DEBUG_PAGE
+extern "C" int l4_debug_pages(unsigned* pk, unsigned* pv, unsigned* meta, int n) {
+  int e = (int)cudaMemcpyFromSymbol(pk, g_pk, sizeof(unsigned) * (size_t)n);
+  if (!e) e = (int)cudaMemcpyFromSymbol(pv, g_pv, sizeof(unsigned) * (size_t)n);
+  if (!e) e = (int)cudaMemcpyFromSymbol(meta, g_pmeta, sizeof(uint4) * (size_t)n);
+  return e;
+}
+#endif
 #ifdef L4_TRACE
 extern "C" int l4_trace_read(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (size_t)n);
@@ -1682,6 +1802,24 @@ extern "C" l4_status l4_decode_workspace_init(const l4_decode_params* p, void* w
     cudaGetLastError();
     return L4_ERR_CUDA;
   }
+  return L4_OK;
+}
+
+extern "C" l4_status l4_decode_workspace_regions(const l4_decode_params* p, size_t workspace_bytes,
+                                                 l4_workspace_regions* out) {
+  int G = 0;
+  l4_status s = check_params(p, &G);
+  if (s != L4_OK) return s;
+  L4_CHECK_ARG(out != nullptr, "out is NULL");
+  WsLayout L;
+  if (!ws_layout_from_bytes(p->batch, p->num_kv_heads, G, workspace_bytes, &L))
+    return fail(L4_ERR_WORKSPACE, "workspace too small");
+  out->state_bytes = L.items;
+  out->partial_lse_offset = L.part_lse;
+  out->partial_o_offset = L.part_o;
+  out->end_offset = L.part_o + (size_t)L.items_cap * G * kHeadDim * sizeof(float);
+  out->items_cap = L.items_cap;
+  out->group_size = G;
   return L4_OK;
 }
 

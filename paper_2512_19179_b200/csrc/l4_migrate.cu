@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "l4_internal.h"
@@ -196,18 +197,29 @@ extern "C" l4_status l4_migrate(const l4_kv_view* src, const int32_t* src_pages,
     s = launch_copies(pool_side(src), pool_side(dst), src->page_bytes, src->num_layers, src_pages, dp.data(), n_pages,
                       st);
     if (s != L4_OK) {
-      l4_pool_free(dst_pool, dp.data(), n_pages);
+      // launch_copies enqueues one kernel per kPairsPerLaunch pages: chunks launched before the
+      // failing one still write into the destination pages, so wait for them before the pages
+      // go back to the pool (a failed synchronisation keeps them allocated: never reused while
+      // a copy may still land, and their ids are reported)
+      if (cudaStreamSynchronize(st) == cudaSuccess) {
+        l4_pool_free(dst_pool, dp.data(), n_pages);
+      } else {
+        cudaGetLastError();
+        std::memcpy(dst_pages_out, dp.data(), (size_t)n_pages * sizeof(int32_t));
+      }
       return s;
     }
   }
+  // the destination ids are the caller's from here on, even if recording the event fails
+  std::memcpy(dst_pages_out, dp.data(), (size_t)n_pages * sizeof(int32_t));
   if (done_event) {
     cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(done_event), st);
     if (e != cudaSuccess) {
       set_error("cudaEventRecord: %s", cudaGetErrorString(e));
-      return L4_ERR_CUDA;  // the copy is enqueued; pages stay allocated for the caller to track
+      cudaGetLastError();
+      return L4_ERR_CUDA;  // the copy is enqueued; dst_pages_out holds the (allocated) pages
     }
   }
-  std::memcpy(dst_pages_out, dp.data(), (size_t)n_pages * sizeof(int32_t));
   return L4_OK;
 }
 
@@ -250,16 +262,15 @@ namespace {
 typedef int (*PFN_getAddressRange)(unsigned long long*, size_t*, unsigned long long);
 PFN_getAddressRange address_range_fn() {
   static PFN_getAddressRange fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;  // first calls from several host threads are safe
+  std::call_once(once, [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<PFN_getAddressRange>(p);
     cudaGetLastError();
-  }
+  });
   return fn;
 }
 }  // namespace

@@ -22,7 +22,8 @@ L4_DECODE_EARLY_INPUTS = 1
 _STATUS_NAMES = ["OK", "INVALID_ARG", "UNSUPPORTED", "CUDA", "WORKSPACE", "NO_PAGES", "INFEASIBLE"]
 
 EXPORTED_SYMBOLS = (
-    "l4_last_error", "l4_version", "l4_decode_workspace_size", "l4_decode_workspace_init", "l4_decode_plan", "l4_decode_run",
+    "l4_last_error", "l4_version", "l4_decode_workspace_size", "l4_decode_workspace_init",
+    "l4_decode_workspace_regions", "l4_decode_plan", "l4_decode_run",
     "l4_decode_attention", "l4_decode_plan_info", "l4_decode_plan_items", "l4_decode_validate", "l4_partition", "l4_pool_create",
     "l4_pool_alloc", "l4_pool_free", "l4_pool_num_free", "l4_pool_destroy", "l4_migrate", "l4_copy_pages",
     "l4_pack_pages", "l4_unpack_pages", "l4_ipc_get_handle", "l4_ipc_open_handle", "l4_ipc_close_handle",
@@ -51,6 +52,12 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("num_items", ctypes.c_int32), ("chunk_pages", ctypes.c_int32), ("num_ctas", ctypes.c_int32),
                 ("max_splits", ctypes.c_int32), ("tail_requests", ctypes.c_int32),
                 ("tail_chunk_pages", ctypes.c_int32)]
+
+
+class WorkspaceRegions(ctypes.Structure):
+    _fields_ = [("state_bytes", ctypes.c_uint64), ("partial_lse_offset", ctypes.c_uint64),
+                ("partial_o_offset", ctypes.c_uint64), ("end_offset", ctypes.c_uint64),
+                ("items_cap", ctypes.c_int32), ("group_size", ctypes.c_int32)]
 
 
 class Stage(ctypes.Structure):
@@ -95,6 +102,8 @@ def lib() -> ctypes.CDLL:
     L.l4_decode_workspace_size.argtypes = [P(DecodeParams), i64]
     L.l4_decode_workspace_init.restype = ctypes.c_int
     L.l4_decode_workspace_init.argtypes = [P(DecodeParams), vp, sz, vp]
+    L.l4_decode_workspace_regions.restype = ctypes.c_int
+    L.l4_decode_workspace_regions.argtypes = [P(DecodeParams), sz, P(WorkspaceRegions)]
     L.l4_decode_plan.restype = ctypes.c_int
     L.l4_decode_plan.argtypes = [P(DecodeParams), vp, vp, i64, vp, sz, vp]
     L.l4_decode_run.restype = ctypes.c_int
@@ -209,6 +218,23 @@ def workspace_init(params: DecodeParams, workspace, stream=None) -> None:
     """l4_decode_workspace_init: zero the scheduler header and split counters of a workspace."""
     _check(lib().l4_decode_workspace_init(ctypes.byref(params), _ptr(workspace), workspace.numel(),
                                           _stream_handle(stream)))
+
+
+def workspace_regions(params: DecodeParams, workspace_bytes: int) -> WorkspaceRegions:
+    """l4_decode_workspace_regions: byte offsets of the scheduler state and the split partials."""
+    r = WorkspaceRegions()
+    _check(lib().l4_decode_workspace_regions(ctypes.byref(params), int(workspace_bytes), ctypes.byref(r)))
+    return r
+
+
+def poison_partials(params: DecodeParams, workspace, stream=None) -> None:
+    """Debug: fill the split-partial region of a workspace with NaN (0xff bytes), so a combine
+    that reads a partial before its split wrote it produces NaN (tests only)."""
+    import torch
+    r = workspace_regions(params, workspace.numel())
+    s = stream if stream is not None else torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        workspace[r.partial_lse_offset:r.end_offset].fill_(0xFF)
 
 
 def decode_plan(params: DecodeParams, kv_len, page_indptr, total_pages: int, workspace, stream=None):

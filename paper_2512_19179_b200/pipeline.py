@@ -19,8 +19,16 @@ cross-GPU traffic is KV-page migration (north star).  The data path of each step
 decode attention over the local batch and the page pack/unpack — runs in libl4 kernels;
 the transport is torch.distributed send/recv (NCCL over NVLink on GPUs).
 
-Within a stage the receiving rank is the least-loaded one by resident tokens (a simple
-stand-in for the bid-ask protocol, which is a next step).
+Within a stage the receiving rank is chosen by the configured policy (least-loaded, the
+bid-ask rule of P:395-399, or round-robin).  Boundaries between stages are refined every
+``refine_every`` steps (§4.3): each instance calls l4_refine_boundary (host C++) on
+the replicated state, so every rank computes the same new boundaries without messages.
+
+Device side (DeviceOps): KV-page transfers run on a dedicated copy stream that waits for the
+step's decode and overlaps the next one; a step's decode waits for the copy stream only
+when a handed-over request joins this rank's batch.  Pages freed in a step return to the
+allocator only after the kernels that may still read them (that step's decode, or the copy
+that sends them) have completed.
 """
 from __future__ import annotations
 
@@ -114,7 +122,8 @@ class ClusterSim:
     def __init__(self, stages, concurrency: int, seed: int = 0, token_budget: int = 1_200_000,
                  batch_cap: int = 1024, max_transfers: int = 3, precopy_lead: int = 0,
                  policy: str = "least_loaded", rebalance_every: int = 0, overload_factor: float = 1.25,
-                 migrate_Bps: float = 7.7e11, kv_bytes_per_token: int = 131072):
+                 migrate_Bps: float = 7.7e11, kv_bytes_per_token: int = 131072, refine_every: int = 0,
+                 qoe_d=None, refine_alpha: float = 0.3, min_traffic: int = 5):
         self.stages = [(int(lo), int(hi), int(m)) for lo, hi, m in stages]
         # receiver choice within a stage: "least_loaded", "bidask" or "round_robin";
         # intra-stage rebalancing of overloaded instances every `rebalance_every` steps
@@ -135,6 +144,17 @@ class ClusterSim:
         self.rank_stage = np.array(assign_ranks(self.stages), dtype=np.int64)
         self.n_ranks = len(self.rank_stage)
         self.stage_hi = np.array([hi for _, hi, _ in self.stages], dtype=np.int64)
+        # NEXT#2 adaptive range refinement: every instance owns the upper boundary of
+        # its range (initialised from the offline plan), refined every `refine_every`
+        # steps from its own and its successors' (I, L) sets; a request hands over when its
+        # length reaches its instance's boundary.  Arrivals route by stage bounds = the mean of
+        # the stage's instance boundaries (reading Z43).
+        self.refine_every = int(refine_every)
+        self.qoe_d = tuple(qoe_d) if qoe_d is not None else None
+        self.refine_alpha, self.min_traffic = float(refine_alpha), int(min_traffic)
+        self.rank_hi = self.stage_hi[self.rank_stage].astype(np.float64)
+        self.bounds = self.stage_hi.astype(np.float64)           # routing upper bound per stage
+        self.refinements = 0
         self.last_stage = len(self.stages) - 1
         self.stage_ranks = [[r for r in range(self.n_ranks) if self.rank_stage[r] == k] for k in range(len(self.stages))]
         self.token_budget = token_budget      # admission limit per instance (KV memory)
@@ -167,10 +187,19 @@ class ClusterSim:
     # ---------------------------------------------------------------- routing
     def stage_of(self, L: int) -> int:
         """Earliest stage whose range covers length L; the last stage takes the rest."""
-        for k, (lo, hi, _) in enumerate(self.stages):
-            if lo <= L < hi:
+        for k in range(self.last_stage):
+            if L < self.bounds[k]:
                 return k
         return self.last_stage
+
+    def current_stages(self):
+        """(lo, hi, instances) with the current (refined) routing bounds, rounded down."""
+        out, lo = [], 0
+        for k, (_, hi, m) in enumerate(self.stages):
+            h = int(hi) if k == self.last_stage else int(math.floor(self.bounds[k]))
+            out.append((lo, h, m))
+            lo = h
+        return out
 
     def _fits(self, r: int, extra_tokens: int) -> bool:
         return self.count[r] < self.batch_cap and self.tokens[r] + extra_tokens <= self.token_budget
@@ -253,7 +282,7 @@ class ClusterSim:
         act = self.active
         st = self.rank_stage[np.maximum(self.rank, 0)]
         nonlast = act & (st != self.last_stage)
-        hi = self.stage_hi[st]
+        hi = self.rank_hi[np.maximum(self.rank, 0)]               # the instance's own boundary
         cand = np.nonzero(nonlast & (self.L >= hi))[0]
         inflight = np.zeros(self.n_ranks, dtype=np.int64)   # transfers in flight per sender
         for ses in self.sessions.values():
@@ -268,7 +297,7 @@ class ClusterSim:
                 if inflight[src] >= self.max_transfers:    # keep running on the source
                     ev.deferred += 1
                     continue
-                dst = self.least_loaded(self.stage_of(L), L)
+                dst = self.least_loaded(self.next_stage(int(self.rank_stage[src]), L), L)
                 if dst is None:                            # no idle cache downstream: skip
                     ev.deferred += 1
                     continue
@@ -283,7 +312,8 @@ class ClusterSim:
                 rid, src, L = int(self.rid[i]), int(self.rank[i]), int(self.L[i])
                 if rid in self.sessions or inflight[src] >= self.max_transfers:
                     continue
-                dst = self.least_loaded(self.stage_of(int(hi[i])), L + self.precopy_lead)
+                dst = self.least_loaded(self.next_stage(int(self.rank_stage[src]), int(math.ceil(hi[i]))),
+                                        L + self.precopy_lead)
                 if dst is None:
                     continue
                 npg = -(-L // PAGE)
@@ -293,6 +323,9 @@ class ClusterSim:
         # 3c. intra-stage rebalancing of overloaded instances via bid-ask
         if self.rebalance_every > 0 and self.step_no % self.rebalance_every == 0:
             self._rebalance(ev, inflight)
+        # 3d. adaptive range refinement
+        if self.refine_every > 0 and self.step_no % self.refine_every == 0:
+            self.refine()
         # 4. arrivals: queued first, then one new request per retirement
         pending, self.queue = self.queue, []
         for _ in range(len(done)):
@@ -302,6 +335,40 @@ class ClusterSim:
             if r is not None:
                 ev.admitted.append((rid, r, I))
         return ev
+
+    def next_stage(self, k: int, L: int) -> int:
+        """Destination stage of a request leaving stage k with length L: the next stage, or a
+        later one when L already lies beyond it."""
+        return min(self.last_stage, max(k + 1, self.stage_of(L)))
+
+    def refine(self):
+        """§4.3 on every instance of every non-last stage: l4_refine_boundary over the
+        instance's (I, L) list and its successors' (the next stage's instances), EMA-smoothed and
+        frozen below `min_traffic` requests; the result clamps to (stage lo, successor hi).  The
+        same host code on the same replicated state gives every rank the same boundaries."""
+        from . import l4
+        if self.qoe_d is None:
+            import synth
+            self.qoe_d = synth.roofline_qoe_d()
+        act = np.nonzero(self.active)[0]
+        per_rank = [[] for _ in range(self.n_ranks)]
+        for i in act:
+            per_rank[int(self.rank[i])].append((int(self.I[i]), int(self.L[i])))
+        new_hi = self.rank_hi.copy()
+        for k in range(self.last_stage):
+            lo = 0 if k == 0 else int(math.floor(self.bounds[k - 1]))
+            hi = int(self.stage_hi[-1]) if k + 1 == self.last_stage else int(math.ceil(self.bounds[k + 1]))
+            if hi - lo < 2:
+                continue
+            succ = [per_rank[r] for r in self.stage_ranks[k + 1]]
+            for r in self.stage_ranks[k]:
+                nb, _, _ = l4.refine_boundary(float(self.rank_hi[r]), per_rank[r], succ, self.qoe_d,
+                                              alpha=self.refine_alpha, min_traffic=self.min_traffic, lo=lo, hi=hi)
+                new_hi[r] = nb
+        self.rank_hi = new_hi
+        for k in range(self.last_stage):
+            self.bounds[k] = float(np.mean([self.rank_hi[r] for r in self.stage_ranks[k]]))
+        self.refinements += 1
 
     def _move(self, i, src, dst, L):
         self.tokens[src] -= L
@@ -358,7 +425,7 @@ class ClusterSim:
         order = np.argsort(self.rid[idx])
         data = np.stack([self.rid[idx][order], self.L[idx][order], self.rank[idx][order]]).astype(np.int64)
         h = 1469598103934665603
-        for x in data.ravel().tolist():
+        for x in data.ravel().tolist() + self.rank_hi.view(np.int64).tolist():
             h = ((h ^ (x & 0xFFFFFFFF)) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
         return h
 
@@ -450,10 +517,17 @@ class RankRuntime:
                    if lists else np.zeros(0, dtype=np.int32))
         return kv_len, indptr, indices
 
+    def reset_stats(self):
+        for k in self.stats:
+            self.stats[k] = 0
+        if hasattr(self.ops, "reset_transfer_stats"):
+            self.ops.reset_transfer_stats()
+
     def apply(self, ev: StepEvents, comm):
         """Apply one step's events to this rank: retire, grow page lists (new tokens),
         migrate KV pages out/in (P2P), admit new requests."""
         me = self.rank
+        free_sent = getattr(self.ops, "free_after_transfer", self.ops.free)
         for rid, r in ev.retired:
             if r == me and rid in self.pages:
                 self.ops.free(self.pool, self._drop(rid))
@@ -498,11 +572,12 @@ class RankRuntime:
                 pages = pages + self.ops.alloc(self.pool, need - len(pages))
                 recvs.append((src, pages[first:need]))
                 done_in.append((rid, pages))
-        nbytes = self.ops.transfer(self.pool, sends, recvs, comm, any_transfer=bool(ev.precopies or ev.migrations))
+        nbytes = self.ops.transfer(self.pool, sends, recvs, comm, any_transfer=bool(ev.precopies or ev.migrations),
+                                   joins=len(done_in), sent=len(done_out))
         for rid, pages in done_in:
             self._add(rid, pages)
         for pages in done_out:
-            self.ops.free(self.pool, pages)
+            free_sent(self.pool, pages)
             self.stats["migrations_out"] += 1
             self.stats["migrated_pages"] += len(pages)
         self.stats["migrations_in"] += len(done_in)
@@ -552,7 +627,15 @@ class H2DRing:
 
 class DeviceOps:
     """libl4 on CUDA: page pool (host allocator over a device KV pool), attention, and the
-    KV-page transport (l4_pack_pages -> NCCL send/recv -> l4_unpack_pages)."""
+    KV-page transport (l4_pack_pages -> NCCL send/recv -> l4_unpack_pages, or one-sided
+    l4_copy_pages pushes over CUDA IPC) on a dedicated copy stream.
+
+    Ordering (NEXT#1): the copy stream first waits for everything enqueued on the compute
+    stream so far (this step's decode and token writes), so a transfer overlaps the NEXT step's
+    decode; that decode waits for the copy stream only when a handed-over request joins this
+    rank's batch (before_decode).  Freed pages are returned to the allocator only after the
+    event that covers their last reader completed: this step's decode (after_decode) for retired
+    requests, the copy for pages that were sent (a receiver writes into idle slots only)."""
 
     def __init__(self, shape, device, seed=0):
         import torch
@@ -560,6 +643,14 @@ class DeviceOps:
         self.torch, self.l4, self.shape, self.device = torch, l4, shape, device
         self.seed = seed
         self.h2d = H2DRing(device)
+        self.copy_stream = torch.cuda.Stream(device=device)
+        self.decode_ev = None          # event after the current step's decode (after_decode)
+        self.copy_ev = None            # event after the last transfer on the copy stream
+        self.join_wait = False         # the next decode must wait for the copy stream
+        self.keep = []                 # (event, buffers) staging kept alive until the copy completed
+        self.timeline = []             # (copy start, copy end, bytes, joins, decode-end event of the step)
+        self.peer_events = {}          # IPC transport: peers' interprocess events
+        self.pending_peers = set()
 
     def make_pool(self, num_pages):
         torch = self.torch
@@ -571,13 +662,37 @@ class DeviceOps:
             for a in range(0, num_pages, 8192):
                 e = min(num_pages, a + 8192)
                 x[a:e] = torch.randn(e - a, *x.shape[1:], device=self.device, generator=g).to(torch.bfloat16)
-        return dict(k=k, v=v, alloc=self.l4.PagePool(num_pages), view=self.l4.kv_view(k, v))
+        return dict(k=k, v=v, alloc=self.l4.PagePool(num_pages), view=self.l4.kv_view(k, v), pending=[])
+
+    # ---------------------------------------------------------------- page ownership
+    def _reclaim(self, pool, block=False):
+        keep = []
+        for ev, pages in pool["pending"]:
+            if ev is None or ev.query() or block:
+                if block and ev is not None:
+                    ev.synchronize()
+                pool["alloc"].free(pages)
+            else:
+                keep.append((ev, pages))
+        pool["pending"] = keep
 
     def alloc(self, pool, n):
-        return pool["alloc"].alloc(n).tolist()
+        self._reclaim(pool)
+        try:
+            return pool["alloc"].alloc(n).tolist()
+        except self.l4.NoPagesError:
+            self._reclaim(pool, block=True)        # wait for the readers of the deferred pages
+            return pool["alloc"].alloc(n).tolist()
 
     def free(self, pool, pages):
-        pool["alloc"].free(pages)
+        """Pages of a retired request: reusable once this step's decode (which read them) completed."""
+        if pages:
+            pool["pending"].append((self.decode_ev, list(pages)))
+
+    def free_after_transfer(self, pool, pages):
+        """Pages sent to another instance: reusable once the copy that reads them completed."""
+        if pages:
+            pool["pending"].append((self.copy_ev if self.copy_ev is not None else self.decode_ev, list(pages)))
 
     def make_table(self, slots, max_pages):
         return self.torch.zeros(slots * max_pages, dtype=self.torch.int32, device=self.device)
@@ -587,20 +702,88 @@ class DeviceOps:
         p, v = self.h2d.put(pos, val)
         table.index_copy_(0, p.long(), v)
 
+    # ---------------------------------------------------------------- step hooks (bench loop)
+    def before_decode(self):
+        """The step's decode waits for pages that landed for requests joining this rank."""
+        cur = self.torch.cuda.current_stream(self.device)
+        if self.join_wait and self.copy_ev is not None:
+            cur.wait_event(self.copy_ev)
+        for src in sorted(self.pending_peers):     # IPC: the senders' copy streams
+            cur.wait_event(self.peer_events[src])
+        self.join_wait = False
+        self.pending_peers = set()
+
+    def after_decode(self, ev, ev_start=None):
+        """`ev` is recorded after this step's decode (and `ev_start` before it): frees of this
+        step wait for it, and the previous step's copy segment is matched to this decode window."""
+        self.decode_ev = ev
+        if ev_start is not None and self.timeline and self.timeline[-1][4] is None:
+            self.timeline[-1][4] = (ev_start, ev)
+        self.keep = [(e, b) for e, b in self.keep if not e.query()]
+
+    def drain(self):
+        self.copy_stream.synchronize()
+        self.torch.cuda.current_stream(self.device).wait_stream(self.copy_stream)
+
+    def reset_transfer_stats(self):
+        self.timeline = []
+
+    def transfer_stats(self):
+        """Copy-stream timing of the transfers since the last reset: per step with a transfer, the
+        copy segment (start..end) against the NEXT step's decode window on the compute stream."""
+        out = dict(copy_ms_sum=0.0, copy_bytes=0, stall_ms_sum=0.0, stall_count=0, stall_ms_max=0.0,
+                   overlap_steps=0)
+        for i, (c0, c1, nb, joins, d_next) in enumerate(self.timeline):
+            dt = c0.elapsed_time(c1)
+            out["copy_ms_sum"] += dt
+            out["copy_bytes"] += nb
+            if joins:                           # a handed-over request waits for this segment
+                out["stall_ms_sum"] += dt
+                out["stall_count"] += joins
+                out["stall_ms_max"] = max(out["stall_ms_max"], dt)
+            if d_next is not None:
+                d0, d1 = d_next
+                if c0.elapsed_time(d1) > 0 and d0.elapsed_time(c1) > 0:   # copy window meets next decode
+                    out["overlap_steps"] += 1
+        return out
+
+    def _segment_begin(self):
+        torch = self.torch
+        cs = self.copy_stream
+        cs.wait_stream(torch.cuda.current_stream(self.device))     # after this step's decode / writes
+        c0 = torch.cuda.Event(enable_timing=True)
+        c0.record(cs)
+        return c0
+
+    def _segment_end(self, c0, nbytes, joins, stalled=None):
+        """Close a copy-stream segment; `joins` > 0: the next decode must wait for it; `stalled`:
+        handed-over requests whose stop round this segment carries (the stall statistic)."""
+        stalled = joins if stalled is None else stalled
+        torch = self.torch
+        c1 = torch.cuda.Event(enable_timing=True)
+        c1.record(self.copy_stream)
+        self.copy_ev = c1
+        if joins:
+            self.join_wait = True
+        self.timeline.append([c0, c1, nbytes, int(stalled), None])
+
     # ---------------------------------------------------------------- one-sided (CUDA IPC)
     def setup_ipc(self, pool, rank: int, world: int, group=None):
         """Map every peer's KV pools into this process (CUDA IPC; handles + offsets travel over
-        the CPU process group `group`).  Afterwards transfer() pushes pages one-sidedly."""
+        the CPU process group `group`), and exchange interprocess events that mark the end of each
+        peer's pushes.  Afterwards transfer() pushes pages one-sidedly."""
         import torch.distributed as dist
-        l4 = self.l4
+        torch, l4 = self.torch, self.l4
         hk, ok = l4.ipc_get_handle(pool["k"].data_ptr())
         hv, ov = l4.ipc_get_handle(pool["v"].data_ptr())
-        mine = (hk, ok, hv, ov)
+        self.my_ipc_event = torch.cuda.Event(interprocess=True)
+        self.my_ipc_event.record(self.copy_stream)
+        mine = (hk, ok, hv, ov, bytes(self.my_ipc_event.ipc_handle()))
         peers = [None] * world
         dist.all_gather_object(peers, mine, group=group)
         view = pool["view"]
         self.ipc_group, self.ipc_rank, self.ipc_views, self.ipc_bases = group, rank, {}, []
-        for r, (pk, pok, pv, pov) in enumerate(peers):
+        for r, (pk, pok, pv, pov, pev) in enumerate(peers):
             if r == rank:
                 continue
             bk, bv = l4.ipc_open_handle(pk), l4.ipc_open_handle(pv)
@@ -608,17 +791,21 @@ class DeviceOps:
             self.ipc_views[r] = l4.kv_view(None, None, device=view.device, num_layers=view.num_layers,
                                            num_pages=view.num_pages, layer_stride_bytes=view.layer_stride_bytes,
                                            page_bytes=view.page_bytes, k_ptr=bk + pok, v_ptr=bv + pov)
+            self.peer_events[r] = torch.cuda.Event.from_ipc_handle(self.device, pev)
 
     def close_ipc(self):
+        self.drain()
         for b in getattr(self, "ipc_bases", []):
             self.l4.ipc_close_handle(b)
         self.ipc_bases, self.ipc_views = [], {}
 
-    def _transfer_ipc(self, pool, sends, recvs, any_transfer):
+    def _transfer_ipc(self, pool, sends, recvs, any_transfer, joins, sent):
         """One-sided: the receivers' destination page lists (allocated in their idle slots)
         reach the senders over the CPU group; each sender writes its pages straight into the
-        receiver's pool (l4_copy_pages over the IPC mapping; NVLink across GPUs), then a
-        barrier publishes them.  Every rank takes part whenever any rank transfers."""
+        receiver's pool on its copy stream (l4_copy_pages over the IPC mapping; NVLink across GPUs,
+        P:426) and records its interprocess event; a barrier publishes the records, and a receiver
+        whose batch gains a handed-over request makes its next decode wait for those senders'
+        events.  Every rank takes part whenever any rank transfers."""
         import torch.distributed as dist
         if not any_transfer:
             return 0
@@ -631,47 +818,61 @@ class DeviceOps:
                 queue.setdefault((src, r), []).append(pages)
         pb = pool["view"].page_bytes
         nbytes = 0
-        for dst, pages in sends:
-            dpages = queue[(me, dst)].pop(0)
-            assert len(dpages) == len(pages)
-            if pages:
-                self.l4.copy_pages(pool["view"], pages, self.ipc_views[dst], dpages)
-            nbytes += len(pages) * 2 * pb
+        c0 = self._segment_begin()
+        with self.torch.cuda.stream(self.copy_stream):
+            for dst, pages in sends:
+                dpages = queue[(me, dst)].pop(0)
+                assert len(dpages) == len(pages)
+                if pages:
+                    self.l4.copy_pages(pool["view"], pages, self.ipc_views[dst], dpages, stream=self.copy_stream)
+                nbytes += len(pages) * 2 * pb
+            self.my_ipc_event.record(self.copy_stream)
+        self._segment_end(c0, nbytes, 0, stalled=sent)   # the sender's segment carries the stop rounds
         nbytes += sum(len(p) for _, p in recvs) * 2 * pb
-        self.torch.cuda.current_stream().synchronize()   # the pushes have landed
-        dist.barrier(group=self.ipc_group)
+        dist.barrier(group=self.ipc_group)                 # every sender recorded its event
+        if joins:
+            self.pending_peers |= {src for src, pages in recvs if pages}
         return nbytes
 
-    def transfer(self, pool, sends, recvs, comm, any_transfer=None):
+    def transfer(self, pool, sends, recvs, comm, any_transfer=None, joins=0, sent=0):
         """sends = [(dst rank, src page ids)], recvs = [(src rank, dst page ids)] in the global
         event order: pack -> batched NCCL P2P -> unpack straight into the receiver's pages
-        (allocated by the caller in idle slots), or the one-sided IPC push after
-        setup_ipc().  Returns bytes moved by this rank."""
+        (allocated by the caller in idle slots), on the copy stream, or the one-sided IPC
+        push after setup_ipc().  joins: handed-over requests entering this rank's batch next step
+        (their decode waits for this copy); sent: handed-over requests this rank sends.
+        Returns bytes moved by this rank."""
         torch, l4, dist = self.torch, self.l4, comm
         if getattr(self, "ipc_views", None) is not None and hasattr(self, "ipc_rank"):
             return self._transfer_ipc(pool, sends, recvs,
-                                      any_transfer if any_transfer is not None else bool(sends or recvs))
+                                      any_transfer if any_transfer is not None else bool(sends or recvs), joins, sent)
         if not sends and not recvs:
             return 0
         pb = pool["view"].page_bytes
         # NCCL moves device buffers over NVLink; the gloo backend (development: several ranks
         # sharing one GPU) needs host buffers, so the staging goes through host memory there.
         host = dist.get_backend() == "gloo"
-        ops, bufs, nbytes = [], [], 0
-        for dst, pages in sends:
-            st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device=self.device)
-            if pages:
-                l4.pack_pages(pool["view"], pages, st)
-            ops.append(dist.P2POp(dist.isend, st.cpu() if host else st, dst))
-            nbytes += len(pages) * 2 * pb
-        for src, pages in recvs:
-            st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device="cpu" if host else self.device)
-            ops.append(dist.P2POp(dist.irecv, st, src))
-            bufs.append((pages, st))
-            nbytes += len(pages) * 2 * pb
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        for pages, st in bufs:
-            if pages:
-                l4.unpack_pages(pool["view"], pages, st.to(self.device) if host else st)
+        ops, bufs, keep, nbytes = [], [], [], 0
+        c0 = self._segment_begin()
+        cs = self.copy_stream
+        with torch.cuda.stream(cs):
+            for dst, pages in sends:
+                st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device=self.device)
+                if pages:
+                    l4.pack_pages(pool["view"], pages, st, stream=cs)
+                ops.append(dist.P2POp(dist.isend, st.cpu() if host else st, dst))
+                keep.append(st)
+                nbytes += len(pages) * 2 * pb
+            for src, pages in recvs:
+                st = torch.empty(max(len(pages), 1) * 2 * pb, dtype=torch.uint8, device="cpu" if host else self.device)
+                ops.append(dist.P2POp(dist.irecv, st, src))
+                bufs.append((pages, st))
+                keep.append(st)
+                nbytes += len(pages) * 2 * pb
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()                         # NCCL: the copy stream waits; the host does not
+            for pages, st in bufs:
+                if pages:
+                    l4.unpack_pages(pool["view"], pages, st.to(self.device) if host else st, stream=cs)
+        self._segment_end(c0, nbytes, joins)
+        self.keep.append((self.copy_ev, keep))   # staging buffers live until the copy completed
         return nbytes

@@ -64,7 +64,7 @@ class MockOps:
     def free(self, pool, pages):
         pool["alloc"].free(pages)
 
-    def transfer(self, pool, sends, recvs, comm, any_transfer=None):
+    def transfer(self, pool, sends, recvs, comm, any_transfer=None, joins=0, sent=0):
         ops, bufs, nbytes = [], [], 0
         for dst, pages in sends:
             idx = torch.tensor(pages, dtype=torch.long)
@@ -86,13 +86,15 @@ class MockOps:
         return nbytes
 
 
-def _worker(rank, world, port, stages, steps, out_q, lead=0, policy="least_loaded", rebalance_every=0):
+def _worker(rank, world, port, stages, steps, out_q, lead=0, policy="least_loaded", rebalance_every=0,
+            refine_every=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         sim = pipeline.ClusterSim(stages, concurrency=48 * world, seed=5, token_budget=400_000, batch_cap=256,
-                                  precopy_lead=lead, policy=policy, rebalance_every=rebalance_every)
+                                  precopy_lead=lead, policy=policy, rebalance_every=rebalance_every,
+                                  refine_every=refine_every)
         ops = MockOps()
         rt = pipeline.RankRuntime(sim, rank, num_pages=400_000 // 16 * 2, shape=None, ops=ops)
         pool = rt.pool
@@ -124,8 +126,9 @@ def _worker(rank, world, port, stages, steps, out_q, lead=0, policy="least_loade
             used = sum(len(p) for p in rt.pages.values()) + sum(len(p) for p in rt.incoming.values())
             assert pool["alloc"].num_free() == pool["alloc"].num_pages - used
         fps = [None] * world
-        dist.all_gather_object(fps, sim.fingerprint())
-        out_q.put((rank, len(set(fps)) == 1, checked, rt.stats))
+        dist.all_gather_object(fps, (sim.fingerprint(), sim.rank_hi.tolist(), sim.refinements))
+        out_q.put((rank, len(set(repr(f) for f in fps)) == 1, checked, dict(rt.stats, rank_hi=sim.rank_hi.tolist(),
+                                                                           refinements=sim.refinements)))
     finally:
         dist.destroy_process_group()
 
@@ -217,3 +220,56 @@ def test_bidask_balances_stages_fig16():
                     cvs.append(np.mean(sim.stage_cv()))
         res[name] = float(np.mean(cvs))
     assert res["full"] < res["inter"] < res["rr"], res
+
+
+def test_pipeline_gloo_refinement_moves_boundaries_and_ranks_agree():
+    """NEXT#2 in the running pipeline: every 10 steps each instance refines its range
+    boundary on the replicated state; over 120 steps the boundaries move, every rank computes the
+    same boundaries, and handovers follow them with pages intact."""
+    world = 3
+    stages = [(0, 1500, 1), (1500, 262144, world - 1)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, stages, 120, q, 0, "least_loaded", 0, 10))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _, _ in res)                         # fingerprint + boundaries agree
+    st = res[0][3]
+    assert st["refinements"] == 12
+    assert st["rank_hi"][0] != 1500.0                              # the first stage's boundary moved
+    assert all(r[3]["rank_hi"] == st["rank_hi"] for r in res)
+    assert sum(r[2] for r in res) > 0                              # migrations happened and were verified
+
+
+def test_sim_refinement_equals_oracle_refine():
+    """The boundary each instance gets from ClusterSim.refine is oracle/refine.py's result on that
+    instance's (I, L) list and its successors' lists, with the stage's outer bounds (Z34-Z37)."""
+    from oracle import refine as orf
+    import synth
+    stages = [(0, 1024, 2), (1024, 8192, 2), (8192, 262144, 1)]
+    sim = pipeline.ClusterSim(stages, concurrency=300, seed=4, token_budget=10 ** 9)
+    for _ in range(30):
+        sim.step()
+    per = [[] for _ in range(sim.n_ranks)]
+    for i in np.nonzero(sim.active)[0]:
+        per[int(sim.rank[i])].append((int(sim.I[i]), int(sim.L[i])))
+    before = sim.rank_hi.copy()
+    bounds = sim.bounds.copy()
+    sim.refine()
+    D = synth.roofline_qoe_d()
+    for k in range(sim.last_stage):
+        lo = 0 if k == 0 else int(np.floor(bounds[k - 1]))
+        hi = int(sim.stage_hi[-1]) if k + 1 == sim.last_stage else int(np.ceil(bounds[k + 1]))
+        succ = [per[r] for r in sim.stage_ranks[k + 1]]
+        for r in sim.stage_ranks[k]:
+            nb, _, _ = orf.refine(before[r], per[r], succ, D, 0.3, 5, lo, hi)
+            assert sim.rank_hi[r] == nb
+    for k in range(sim.last_stage):
+        assert sim.bounds[k] == np.mean([sim.rank_hi[r] for r in sim.stage_ranks[k]])
+    assert sim.rank_hi[-1] == before[-1]                            # the last stage has no upper boundary
