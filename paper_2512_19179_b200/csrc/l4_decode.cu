@@ -134,13 +134,6 @@ __device__ __forceinline__ unsigned long long trace_now() {
 // producer issued, built only into debug variants (-DL4_DEBUG_CKS).
 __device__ unsigned g_cks[16384 * 4];
 #endif
-#ifdef L4_DEBUG_PAGE
-// Development-only per-(page, kv head) record of one call: K / V fragment checksums and where the
-// slice was consumed (CTA, ring sequence number, page index in its item | warp << 16, item).
-constexpr int kDbgPages = 1 << 21;
-__device__ unsigned g_pk[kDbgPages], g_pv[kDbgPages];
-__device__ uint4 g_pmeta[kDbgPages];
-#endif
 
 // Header region (256 B): plan summary + dynamic scheduler state.
 struct __align__(16) PlanHeader {
@@ -804,16 +797,6 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
       mma_bf16_16816(s, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
     }
   }
-#ifdef L4_DEBUG_VEARLY
-  uint32_t vf[8][4];  // experiment: every V fragment read before the softmax
-  {
-    const int tok = r8 + ((mi >> 1) << 3);
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
-      ldmatrix_x4_trans(sbase + kSliceBytes + slice_off(tok, mt * 2 + (mi & 1)), vf[mt][0], vf[mt][1], vf[mt][2],
-                        vf[mt][3]);
-  }
-#endif
   // ---- mask (Z20: tokens >= kv_len are not attended) and online softmax in the exp2 domain
   const float NEG = -INFINITY;
   const float t0 = (g < valid) ? s[0] * scale_log2 : NEG;
@@ -857,12 +840,7 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
       uint32_t a0, a1, a2, a3;
-#ifdef L4_DEBUG_VEARLY
-      a0 = vf[mt][0]; a1 = vf[mt][1]; a2 = vf[mt][2]; a3 = vf[mt][3];
-      (void)vbase; (void)tok;
-#else
       ldmatrix_x4_trans(vbase + slice_off(tok, mt * 2 + (mi & 1)), a0, a1, a2, a3);
-#endif
       if (valid < kPage) {
         a0 &= mlo;
         a1 &= mlo;
@@ -918,11 +896,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < kStages; ++i) s_seq[i] = -1;
     for (int i = 0; i < kStages; ++i) {
       mbar_init(bar_full + i * 8, 1);
-#ifdef L4_DEBUG_ALLARRIVE
-      mbar_init(bar_empty + i * 8, 32);  // experiment: every lane of the consuming warp arrives
-#else
       mbar_init(bar_empty + i * 8, 1);
-#endif
     }
     for (int i = 0; i < kItemSlots; ++i) {
       mbar_init(bar_ifull + i * 8, 1);
@@ -1275,9 +1249,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     return a.counters + (size_t)w.b * a.Hkv + w.h;
   };
   auto finish_group = [&](const WorkItem& w) {  // this CTA was the last split of w's group
-#ifdef L4_DEBUG_FENCE
-    __threadfence();  // experiment: every reader fences before reading the partials
-#endif
     const int ns = w.nsplit;
     const int ng = (ns + kCombineGroup - 1) / kCombineGroup;
     const int g0 = (w.split / kCombineGroup) * kCombineGroup;
@@ -1339,11 +1310,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         mbar_wait(bar_full + st * 8, (q / kStages) & 1);
         load_qf(smem + SL::stages + st * kStageBytes);
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty + st * 8);
         qbase += kQuad;
       } else {
         load_qf(smem + SL::qslots + slot * SL::qslot_bytes + warp * (G * kHeadDim * 2));
+        fence_proxy_async_smem();  // Q-slot reads before the producer's next bulk copy into the slot
         __syncwarp();
         mbar_arrive(bar_iempty + slot * 8);
       }
@@ -1364,6 +1337,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (j < np)
           consume_page(sbase + SL::stages + st * kStageBytes, (j == np - 1) ? it.last_valid : kPage, qf, acc, mrow,
                        lrow, a.scale_log2, lane, cks_k, cks_v);
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty + st * 8);
       }
@@ -1411,6 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
+    fence_proxy_async_smem();  // Q-slot reads before the producer's next bulk copy into the slot
     __syncwarp();
     mbar_arrive(bar_iempty + slot * 8);
 
@@ -1431,9 +1406,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       mbar_wait(bar_full + st * 8, (q / kStages) & 1);
-#ifdef L4_DEBUG_RAW_FENCE
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment: after the wait, before reads
-#endif
 #ifdef L4_TRACE
       if (q == 0 && lane == 0) L4_MARK(4);
       if (warp == 0 && lane == 0) trace_add(12, trace_now() - tw0);
@@ -1442,38 +1414,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef L4_TRACE
       const unsigned long long tc0 = trace_now();
 #endif
-#ifdef L4_DEBUG_PAGE
-      const uint32_t ck0 = cks_k, cv0 = cks_v;
-#endif
       consume_page(sbase + SL::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane, cks_k, cks_v);
-#ifdef L4_DEBUG_PAGE
-      {
-        uint32_t dk = cks_k ^ ck0, dv = cks_v ^ cv0;
-        for (int o = 16; o; o >>= 1) {
-          dk ^= __shfl_xor_sync(0xffffffffu, dk, o);
-          dv ^= __shfl_xor_sync(0xffffffffu, dv, o);
-        }
-        const int page = __ldg(a.indices + it.pbeg + j);
-        const long long key = (long long)page * a.Hkv + it.h;
-        if (lane == 0 && key < kDbgPages) {
-          g_pk[key] = dk;
-          g_pv[key] = dv;
-          g_pmeta[key] = make_uint4(blockIdx.x, q, (unsigned)j | ((unsigned)warp << 16) | ((unsigned)k << 20), item_idx);
-        }
-      }
-#endif
 #ifdef L4_TRACE
       if (warp == 0 && lane == 0) trace_add(11, trace_now() - tc0);
 #endif
+      fence_proxy_async_smem();  // this warp's reads of the stage before the producer's next TMA into it
       __syncwarp();
-#ifdef L4_DEBUG_PROXY_FENCE
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // experiment: generic reads before TMA writes
-#endif
-#ifdef L4_DEBUG_ALLARRIVE
-      mbar_arrive(bar_empty + st * 8);
-#else
       if (lane == 0) mbar_arrive(bar_empty + st * 8);
-#endif
     }
     qbase += np;
     if (early && k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
@@ -1570,9 +1517,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     // Release: bar.sync orders every thread's partial stores before thread 0's acq_rel ticket
     // (cumulative); acquire: the ticket, then bar.sync, then ld.global.cg reads.  An unsplit item
     // with no pending ticket needs only the final barrier (merge area free).
-#ifdef L4_DEBUG_FENCE
-    if (split) __threadfence();  // experiment: every thread fences its own partial stores
-#endif
     if (split || has_pend) named_bar_sync(1, kConsumerThreads);
     if (has_pend && ct == 0) {
       const int last = (pend_old == group_need(pend_it) - 1);
@@ -1766,14 +1710,6 @@ extern "C" int l4_debug_cks(unsigned* host, int n, int clear) {
     return (int)cudaMemset(p, 0, sizeof(unsigned) * 16384 * 4);
   }
   return (int)cudaMemcpyFromSymbol(host, g_cks, sizeof(unsigned) * (size_t)n);
-}
-#endif
-#ifdef L4_DEBUG_PAGE
-extern "C" int l4_debug_pages(unsigned* pk, unsigned* pv, unsigned* meta, int n) {
-  int e = (int)cudaMemcpyFromSymbol(pk, g_pk, sizeof(unsigned) * (size_t)n);
-  if (!e) e = (int)cudaMemcpyFromSymbol(pv, g_pv, sizeof(unsigned) * (size_t)n);
-  if (!e) e = (int)cudaMemcpyFromSymbol(meta, g_pmeta, sizeof(uint4) * (size_t)n);
-  return e;
 }
 #endif
 #ifdef L4_TRACE

@@ -79,6 +79,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// Orders this thread's earlier generic-proxy accesses of shared memory (ldmatrix / ld.shared of a
+// TMA-filled buffer) before async-proxy accesses that follow the release it precedes (the next
+// TMA / bulk copy into the buffer).  Without it a consumer's reads could observe the producer's
+// next copy into the stage (measured: 1 in ~800 C4 calls read a wrong V slice).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- shared-memory flags
 __device__ __forceinline__ void st_release_cta(uint32_t addr, int v) {
   asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");

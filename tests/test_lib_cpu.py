@@ -296,33 +296,3 @@ def test_quad_bin_bound_holds_for_every_chunk():
             largest = -(-p // ns)
             assert 3 * largest > 2 * C
             assert largest.bit_length() > qb  # a split request never lands in a quad bin
-
-
-def test_quad_unit_mapping_covers_every_item_once():
-    """The decode kernel's scheduling units, restated: items [0, n_wide) one per
-    unit, then n_quads units of four consecutive items, then the remainder one per unit; with
-    n_quads = (rest - min(rest, tail x W)) // 4, zeroed below min x W.  Every item belongs to
-    exactly one unit, units are in item order, and quad units are always full."""
-    rng = np.random.default_rng(5)
-    for _ in range(600):
-        W = int(rng.integers(1, 300))
-        n_items = int(rng.integers(0, 20000))
-        n_wide = int(rng.integers(0, n_items + 1))
-        tail, qmin = int(rng.integers(0, 3)), int(rng.integers(1, 6))
-        rest = n_items - n_wide
-        n_quads = (rest - min(rest, tail * W)) // 4
-        if n_quads < qmin * W:
-            n_quads = 0
-        n_units = n_items - 3 * n_quads
-        u_tail = n_wide + n_quads
-
-        def unit_items(u):
-            if u < n_wide:
-                return [u]
-            if u < u_tail:
-                f = n_wide + 4 * (u - n_wide)
-                return [f, f + 1, f + 2, f + 3]
-            return [u + 3 * n_quads]
-
-        seen = [i for u in range(n_units) for i in unit_items(u)]
-        assert seen == list(range(n_items))
