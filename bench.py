@@ -57,6 +57,11 @@ WORKLOADS = {
                     "mixed batch", shape=synth.SHAPE_LLAMA3_8B, lens=lambda: synth.lengths_c3(0)),
     "c4": dict(desc="BASELINE configs[3]: Llama-3-70B attention (64q/8kv), long-context batch 32, 32K..128K (seed 0)",
                shape=synth.SHAPE_LLAMA3_70B, lens=lambda: synth.lengths_c4(0)),
+    # homogeneous short-request batches (extra lines; --workload for profiling runs)
+    "short64": dict(desc="B = 1024 x 64 tokens, Llama-3-8B shape (short-stage batch)", shape=synth.SHAPE_LLAMA3_8B,
+                    lens=lambda: np.full(1024, 64, dtype=np.int64)),
+    "short200": dict(desc="B = 1024 x 200 tokens, Llama-3-8B shape (short-stage batch)", shape=synth.SHAPE_LLAMA3_8B,
+                     lens=lambda: np.full(1024, 200, dtype=np.int64)),
 }
 METRIC = "decode-attn KV GB/s (% HBM peak), mixed vs binned; tokens/s at 1/2/4/8 GPUs"
 L2_BYTES = 126 * (1 << 20)
@@ -1037,7 +1042,7 @@ def main(argv=None):
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c4", "short64", "short200"])
     ap.add_argument("--impl", default="l4", choices=["l4", "reference"])
     ap.add_argument("--copies", type=int, default=4, help="rotating input copies (L2 rotation)")
     ap.add_argument("--no-extra", action="store_true", help="skip the extra lines (C4, C2, binned, short, fig2)")

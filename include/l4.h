@@ -88,7 +88,7 @@ typedef struct {
   int32_t chunk_pages;    /* 0 = automatic length-binned split; > 0 forces the split
                              chunk C (pages per work item); < 0 = never split.  Requests
                              of <= 2C pages are never split (no combine needed). */
-  int32_t flags;          /* 0 or L4_DECODE_EARLY_INPUTS */
+  int32_t flags;          /* 0, L4_DECODE_EARLY_PLAN or L4_DECODE_EARLY_INPUTS (below) */
 } l4_decode_params;
 
 /* l4_decode_attention (single-launch path) may start reading its INPUTS (q, the KV pools,
@@ -99,6 +99,12 @@ typedef struct {
  * launched immediately before on the same stream cannot be writing those inputs (another
  * l4 call, or any kernel that does not itself trigger programmatic launch early). */
 enum { L4_DECODE_EARLY_INPUTS = 1 };
+/* Weaker form for a decode step's layer loop, where the kernel before attention writes q and the
+ * step's new K/V token but never the page table: only the planner's inputs (kv_len, page_indptr)
+ * are read before the previous kernel completes; q, the KV pools, page_indices, the workspace and
+ * the outputs are touched after it.  Set it only when the kernel launched immediately before on
+ * the same stream cannot be writing kv_len / page_indptr.  L4_DECODE_EARLY_INPUTS implies it. */
+enum { L4_DECODE_EARLY_PLAN = 2 };
 
 /* Bytes of device workspace needed for any batch whose page table has at most
  * max_total_pages entries (indptr[B] <= max_total_pages).  Returns 0 if the

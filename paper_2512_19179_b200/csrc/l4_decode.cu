@@ -208,7 +208,7 @@ l4_status check_params(const l4_decode_params* p, int* G_out) {
   if (!(G == 1 || G == 2 || G == 4 || G == 8)) return fail(L4_ERR_UNSUPPORTED, "GQA group must be 1, 2, 4 or 8");
   L4_CHECK_ARG(p->out_dtype == L4_DT_F32 || p->out_dtype == L4_DT_BF16, "out_dtype must be F32 or BF16");
   L4_CHECK_ARG(std::isfinite(p->sm_scale), "sm_scale must be finite");
-  L4_CHECK_ARG((p->flags & ~L4_DECODE_EARLY_INPUTS) == 0, "unknown decode flags");
+  L4_CHECK_ARG((p->flags & ~(L4_DECODE_EARLY_INPUTS | L4_DECODE_EARLY_PLAN)) == 0, "unknown decode flags");
   *G_out = G;
   return L4_OK;
 }
@@ -582,7 +582,7 @@ struct RunArgs {
   const int* indptr;
   int B, forced_chunk, items_cap;
   int quad_bin;  // kQuadBin (0: no quad units)
-  int early;  // L4_DECODE_EARLY_INPUTS: read inputs before griddepcontrol.wait (fused path)
+  int early;  // 1: L4_DECODE_EARLY_INPUTS, 2: L4_DECODE_EARLY_PLAN (fused path), 0: neither
 };
 
 struct __align__(16) SlotItem {  // unit handed from the producer to the consumers
@@ -917,14 +917,18 @@ __global__ void __launch_bounds__(kThreads, 2)
   // Early mode (fused only): the plan and the first item's loads read only the caller's inputs,
   // which the previous kernel must not be writing (L4_DECODE_EARLY_INPUTS); every access to the
   // workspace and every output write still comes after griddepcontrol.wait.
-  const bool early = kFused && a.early;
-  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Early-plan mode (L4_DECODE_EARLY_PLAN, fused only): the plan reads kv_len / indptr before
+  // the wait (the kernel before must not write them: true in a decode step's layer loop, where
+  // the page table is uploaded once per step), q / K / V and the workspace only after it.
+  const bool early = kFused && a.early == 1;
+  const bool early_plan = kFused && a.early == 2;
+  if (!early && !early_plan) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) L4_MARK(1);
 
   const int W = gridDim.x;
   // producer lane 0: the first three scheduler tickets, in flight while the plan is built
   int raw_t0 = -1, raw_t1 = -1, raw_t2 = -1;
-  if (!early && warp == kConsumerWarps && lane == 0) {
+  if (!early && !early_plan && warp == kConsumerWarps && lane == 0) {
     raw_t0 = atomicAdd(&a.header->sched_next, 1);
     raw_t1 = atomicAdd(&a.header->sched_next, 1);
     raw_t2 = atomicAdd(&a.header->sched_next, 1);
@@ -945,6 +949,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     n_items = a.header->n_items;
     n_wide = SL::quads ? a.header->n_wide : n_items;
     q_pages = a.header->quad_pages;
+  }
+  if (early_plan) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (warp == kConsumerWarps && lane == 0) {
+      raw_t0 = atomicAdd(&a.header->sched_next, 1);
+      raw_t1 = atomicAdd(&a.header->sched_next, 1);
+      raw_t2 = atomicAdd(&a.header->sched_next, 1);
+    }
   }
   // Scheduling units: items [0, n_wide) one per unit (CTA-wide); then the quad-eligible suffix
   // four items per unit (one per consumer warp), except its last kQuadTailPerCta x W items,
@@ -1876,7 +1888,7 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   a.forced_chunk = p->chunk_pages;
   a.items_cap = L.items_cap;
   a.quad_bin = kQuadBin;
-  a.early = fused && (p->flags & L4_DECODE_EARLY_INPUTS) != 0;
+  a.early = !fused ? 0 : (p->flags & L4_DECODE_EARLY_INPUTS) ? 1 : (p->flags & L4_DECODE_EARLY_PLAN) ? 2 : 0;
   if (fused) {
     switch (G) {
       case 1: return launch_decode<1, true>(tk, tv, tq, a, ctas, st);

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("L4_LIB") or os.path.join(_HERE, "libl4.so")  # L4_LIB
 L4_OK, L4_ERR_INVALID_ARG, L4_ERR_UNSUPPORTED, L4_ERR_CUDA, L4_ERR_WORKSPACE, L4_ERR_NO_PAGES, L4_ERR_INFEASIBLE = range(7)
 L4_DT_F32, L4_DT_BF16 = 0, 1
 L4_DECODE_EARLY_INPUTS = 1
+L4_DECODE_EARLY_PLAN = 2
 _STATUS_NAMES = ["OK", "INVALID_ARG", "UNSUPPORTED", "CUDA", "WORKSPACE", "NO_PAGES", "INFEASIBLE"]
 
 EXPORTED_SYMBOLS = (

@@ -56,6 +56,7 @@ def launches(path):
 
 def main(tag="r1", wls=("c2", "c3", "c4")):
     os.makedirs(PROF, exist_ok=True)
+    traffic = {}
     lines = [f"# ncu evidence — {tag}", "",
              "Captured under gpurun on one B200 with `scripts/gpu_round.sh` (`ncu --set full --clock-control none "
              "--import-source on -k regex:<the single-launch decode_kernel<G, true>>`; launch lists with "
@@ -76,6 +77,16 @@ def main(tag="r1", wls=("c2", "c3", "c4")):
                 dur_us /= 1e3
             rd = g("dram__bytes_read.sum")
             wr = g("dram__bytes_write.sum")
+            try:
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+                r_b = float(rd[0].replace(",", "")) * scale.get(rd[1], 1)
+                w_b = float(wr[0].replace(",", "")) * scale.get(wr[1], 1)
+                traffic[wl] = {"traffic": int(r_b + w_b), "dram_read": int(r_b), "dram_write": int(w_b),
+                               "duration_us": round(dur_us, 2),
+                               "kernel": "decode_kernel<G, true> (single-launch l4_decode_attention)",
+                               "source": f"prof_{tag}_{wl}.ncu-rep (ncu --set full)"}
+            except ValueError:
+                pass
             lines.append("")
             lines.append("| metric | value |")
             lines.append("|---|---|")
@@ -103,8 +114,11 @@ def main(tag="r1", wls=("c2", "c3", "c4")):
             shutil.copy(lst, os.path.join(PROF, os.path.basename(lst)))
         lines.append("")
     open(os.path.join(PROF, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
+    if traffic:
+        import json
+        json.dump(traffic, open(os.path.join(PROF, f"{tag}_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["r1"]))
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1", tuple(sys.argv[2:]) or ("c2", "c3", "c4"))

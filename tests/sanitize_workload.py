@@ -52,6 +52,23 @@ for Hq in (32, 64):
     l4.decode_run(pe, qd, kd, vd, ix, o2, l2, ws)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.isfinite(o1).all()
+# split-heavy, C4-like (Llama-3-70B shape: 64 q / 8 kv heads): long requests split up to 38 ways
+# (two-level combine groups of 16), back-to-back early-input calls, NaN-poisoned split partials
+lens = np.array([6000, 9000, 12000, 33])
+shape = synth.AttnShape("s", 64, 8)
+t = synth.make_page_table(lens, seed=3, spare_pages=3)
+q, k, v = synth.make_qkv_cpu(shape, t, seed=3)
+qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+ip, ix, kl = (torch.from_numpy(x).cuda() for x in (t.indptr, t.indices, t.kv_len))
+ref, rl = l4.decode_attention(qd, kd, vd, ip, ix, kl, chunk_pages=20)
+pe = l4.make_params(len(lens), 64, 8, chunk_pages=20, flags=l4.L4_DECODE_EARLY_INPUTS)
+ws = l4.alloc_workspace(pe, t.total_pages)
+l4.poison_partials(pe, ws)
+o1, l1 = torch.empty_like(ref), torch.empty_like(rl)
+for _ in range(3):
+    l4.attention_call(pe, qd, kd, vd, ip, ix, kl, t.total_pages, o1, l1, ws)
+torch.cuda.synchronize()
+assert torch.equal(o1, ref) and torch.equal(l1, rl) and torch.isfinite(o1).all()
 kk = torch.randn(2, 40, 2, 16, 128, device="cuda").to(torch.bfloat16)
 vv = torch.randn_like(kk)
 dk, dv = torch.zeros_like(kk), torch.zeros_like(vv)

@@ -38,10 +38,10 @@ class _Hub:
 
     def batch_isend_irecv(self, ops):
         for o in ops:
-            if o.op is self.isend:
+            if o.op == self.isend:
                 self.mail.setdefault((self.me, o.peer), []).append(o.tensor.clone())
         for o in ops:
-            if o.op is self.irecv:
+            if o.op == self.irecv:
                 o.tensor.copy_(self.mail[(o.peer, self.me)].pop(0))
 
         class _W:
@@ -125,3 +125,113 @@ def test_two_instances_loopback_migration(lead):
     assert n_mig > 0
     for rt in rts:
         _attention_check(rt, shape, q)
+
+
+class _ThreadHub:
+    """torch.distributed's batched P2P for ranks that are threads of one process on one device:
+    a sender records an event on its current (copy) stream, the receiver's copy stream waits for
+    it and copies — device-asynchronous, like NCCL, so copies can overlap kernels."""
+
+    class P2POp:
+        def __init__(self, op, tensor, peer):
+            self.op, self.tensor, self.peer = op, tensor, peer
+
+    def __init__(self, world):
+        import threading
+        self.box, self.bar, self.tls = {}, threading.Barrier(world), threading.local()
+
+    @staticmethod
+    def get_backend():
+        return "nccl"
+
+    def isend(self):
+        pass
+
+    def irecv(self):
+        pass
+
+    def batch_isend_irecv(self, ops):
+        me = self.tls.rank
+        for o in ops:
+            if o.op == self.isend:
+                ev = torch.cuda.Event()
+                ev.record()
+                self.box.setdefault((me, o.peer), []).append((o.tensor, ev))
+        self.bar.wait()
+        for o in ops:
+            if o.op == self.irecv:
+                t, ev = self.box[(o.peer, me)].pop(0)
+                torch.cuda.current_stream().wait_event(ev)
+                o.tensor.copy_(t)
+        self.bar.wait()
+
+        class _W:
+            def wait(self):
+                pass
+        return [_W() for _ in ops]
+
+
+def test_bidirectional_precopy_overlaps_next_decode():
+    """NEXT#1 on the device: in one step rank 0 pre-copies a request to rank 1 and
+    rank 1 pre-copies one to rank 0 (both directions at once), on each rank's copy stream, while
+    both ranks run their next decode; the copy segments overlap those decodes (CUDA event
+    timeline) and every page arrives with its bytes."""
+    import threading
+    shape = synth.AttnShape("t", 8, 2)
+    sim = pipeline.ClusterSim([(0, 1 << 21, 2)], concurrency=24, seed=3, token_budget=10 ** 9, batch_cap=64)
+    hub = _ThreadHub(2)
+    ops = [pipeline.DeviceOps(shape, "cuda", seed=r) for r in range(2)]
+    rts = [pipeline.RankRuntime(sim, r, 200000, shape, ops[r]) for r in range(2)]
+    # the largest resident request of each rank moves to the other one (pre-copy round)
+    pick = {}
+    for r in range(2):
+        rids, Ls = sim.batch(r)
+        pick[r] = (int(rids[int(np.argmax(Ls))]), int(Ls.max()))
+    ev = pipeline.StepEvents()
+    ev.precopies = [(pick[0][0], 0, 1, -(-pick[0][1] // 16)), (pick[1][0], 1, 0, -(-pick[1][1] // 16))]
+    snaps = {r: (rts[r].pool["k"][torch.tensor(rts[r].pages[pick[r][0]], device="cuda")].clone(),
+                 rts[r].pool["v"][torch.tensor(rts[r].pages[pick[r][0]], device="cuda")].clone()) for r in range(2)}
+    q = torch.randn(64, shape.num_q_heads, 128, device="cuda").to(torch.bfloat16)
+    torch.cuda.synchronize()
+    errs = []
+
+    def rank_main(r):
+        try:
+            hub.tls.rank = r
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                rt, op = rts[r], ops[r]
+                for step in range(2):
+                    op.before_decode()
+                    kv_len, indptr = rt.device_batch()
+                    B = len(kv_len)
+                    d_len, d_ptr = (torch.from_numpy(x).cuda() for x in (kv_len, indptr))
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(20):      # a long decode window
+                        l4.decode_attention(q[:B], rt.pool["k"], rt.pool["v"], d_ptr, rt.table, d_len)
+                    e1.record()
+                    op.after_decode(e1, e0)
+                    if step == 0:
+                        rt.apply(ev, hub)
+                op.drain()
+                torch.cuda.synchronize()
+        except BaseException as e:   # noqa
+            errs.append(e)
+            hub.bar.abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    for r in range(2):
+        st = ops[r].transfer_stats()
+        assert st["copy_bytes"] > 0 and st["overlap_steps"] == 1, st
+        other = 1 - r
+        rid = pick[other][0]
+        pages = rts[r].incoming[rid]
+        k0, v0 = snaps[other]
+        idx = torch.tensor(pages, device="cuda")
+        assert torch.equal(rts[r].pool["k"][idx], k0) and torch.equal(rts[r].pool["v"][idx], v0)
