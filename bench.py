@@ -230,15 +230,18 @@ def _call(l4, params, wl, i, ws, stream=None):
     l4.attention_call(params, q, k, v, ip, ix, kl, wl.table.total_pages, wl.out, wl.lse, ws, stream)
 
 
-def steady_ms(wl: Workload, steps: int, warmup: int, early: bool = False):
+def steady_ms(wl: Workload, steps: int, warmup: int, early: bool = False, early_plan: bool = False):
     """Device time per step of `steps` back-to-back l4_decode_attention calls (one event pair
     around them, rotating input copies).  early=False: plain calls (each call starts reading
     after the previous one completed, as after a kernel that writes q); early=True:
     L4_DECODE_EARLY_INPUTS (the next call plans and streams its first item under the previous
-    call's tail).  An event between two launches would stop that overlap, hence one pair."""
+    call's tail); early_plan=True: L4_DECODE_EARLY_PLAN (only the planner's page-table reads run
+    under the previous call's tail).  An event between two launches would stop that overlap,
+    hence one pair."""
     import torch
     from paper_2512_19179_b200 import l4 as _l4
-    l4, params, ws = make_l4(wl, flags=_l4.L4_DECODE_EARLY_INPUTS if early else 0)
+    flags = _l4.L4_DECODE_EARLY_INPUTS if early else (_l4.L4_DECODE_EARLY_PLAN if early_plan else 0)
+    l4, params, ws = make_l4(wl, flags=flags)
     st = torch.cuda.current_stream()
     for i in range(warmup):
         _call(l4, params, wl, i, ws)
@@ -621,6 +624,7 @@ def single_gpu_line(args, rank, world, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t[0])
     early = steady_ms(wl, args.steps, args.warmup, early=True)
+    eplan = steady_ms(wl, args.steps, args.warmup, early_plan=True)
     cold = cold_ms(wl)
     info = plan_of(wl)
     e2e_steps = max(50, args.steps)
@@ -647,6 +651,8 @@ def single_gpu_line(args, rank, world, local):
     roof = {args.workload + "_cold": {"ms": round(cold, 5), "frac": round(wl.bytes_algo / (cold / 1e3) / 1e9 / peak, 4)},
             args.workload + "_early_inputs": {"ms": round(early, 5),
                                               "frac": round(wl.bytes_algo / (early / 1e3) / 1e9 / peak, 4)},
+            args.workload + "_early_plan": {"ms": round(eplan, 5),
+                                            "frac": round(wl.bytes_algo / (eplan / 1e3) / 1e9 / peak, 4)},
             **roof}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -887,11 +893,11 @@ def pipeline_line(args, world, rank, local):
     clocks = ClockSampler(local)
     clocks.start()
     clk = None
-    arms = (("l4", stages, True, 50), ("l4_static", stages, True, 0), ("round_robin", rr, False, 0),
-            ("l4_e2e", stages, True, 50))
+    arms = (("l4", stages, True, 10), ("l4_static", stages, True, 0), ("round_robin", rr, False, 0),
+            ("l4_e2e", stages, True, 10))
     for name, st, l4arm, refine in arms:
         # L4 arm: bid-ask receivers + intra-stage rebalancing, live (two-round)
-        # migration with an 8-token pre-copy lead, boundary refinement every 50 steps
+        # migration with an 8-token pre-copy lead, boundary refinement every 10 steps
         # (P:369-379); l4_static: the same without refinement; baseline: one length-agnostic
         # stage, round-robin placement
         t = run_pipeline_arm(st, args.steps, args.warmup, rank, world, device,

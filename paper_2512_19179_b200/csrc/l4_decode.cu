@@ -96,6 +96,12 @@ constexpr int kQuadTailPerCta = L4_QUAD_TAIL;  // CTA-wide items per CTA at the 
 #define L4_QUAD_MIN 4
 #endif
 constexpr int kQuadMinPerCta = L4_QUAD_MIN;  // quads only if there are at least this many per CTA
+#ifndef L4_TICKET_AHEAD
+#define L4_TICKET_AHEAD 3
+#endif
+// Scheduler tickets a CTA holds beyond its current unit: 3 (two resolved, one in flight; no
+// atomic round trip between units) or 1 (drawn when the current unit's pages are out).
+constexpr int kTicketAhead = L4_TICKET_AHEAD;
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kLog2e = 1.44269504088896340736f;
 
@@ -108,6 +114,7 @@ static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
 // Development-only timeline probe (scripts/trace_fused.py): %globaltimer at fixed points of
 // every CTA, built only into trace variants (scripts/build_variant.sh ... -DL4_TRACE).
 __device__ unsigned long long g_trace[4096 * 16];
+__device__ unsigned long long g_trace_last[4096 * 4];  // last CTA-wide item: start, pages, splits, index
 __device__ __forceinline__ void trace_mark(int k) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -284,7 +291,7 @@ __device__ __forceinline__ int nsplit_of(int pages, int C) {
 
 __device__ __forceinline__ int bin_of(int pages, int nsplit) {
   if (pages <= 0) return 0;
-  const int ip = (pages + nsplit - 1) / nsplit;  // pages of the largest split
+  const int ip = nsplit == 1 ? pages : (pages + nsplit - 1) / nsplit;  // pages of the largest split
   return min(kNumBins - 1, 32 - __clz(ip));      // bit_length(ip)
 }
 
@@ -319,13 +326,25 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   {
     long long sum = 0;
     int mx = 0;
-    for (int b = tid; b < B; b += nthr) {
-      const int L = kv_len[b];
-      s_len[b] = L;
-      s_ptr[b] = indptr[b];
-      const int pg = pages_of(L);
-      sum += pg;
-      mx = max(mx, pg);
+    for (int b0 = tid; b0 < B; b0 += 4 * nthr) {  // four loads of each array in flight per thread
+      int Lv[4], Pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = b0 + u * nthr;
+        Lv[u] = b < B ? kv_len[b] : 0;
+        Pv[u] = b < B ? indptr[b] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = b0 + u * nthr;
+        if (b < B) {
+          s_len[b] = Lv[u];
+          s_ptr[b] = Pv[u];
+          const int pg = pages_of(Lv[u]);
+          sum += pg;
+          mx = max(mx, pg);
+        }
+      }
     }
     for (int x = tid; x < nw * kNumBins; x += nthr) s_wcnt[x] = 0;
     block_reduce3(sum, mx, 0u, s_ll, s_i, s_u, &T, &Pmax, &unused);  // its barriers publish s_len/s_ptr
@@ -355,17 +374,15 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     int wsum = 0, wms = kNumBins;
     for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 1: per-warp bin histogram + item count
       const int b = t0 + lane;
-      int bin = -1;
       if (b < r1) {
         const int pg = pages_of(s_len[b]);
         const int ns = nsplit_of(pg, C);
-        bin = bin_of(pg, ns);
+        const int bin = bin_of(pg, ns);
         wsum += ns;
         if (ns > 1) wms = min(wms, bin);
+        s_off[b] = bin | (ns << 16);              // kept for pass 2 (s_off is free until the scan)
+        atomicAdd(&s_wcnt[warp * kNumBins + bin], 1);  // counts only: iterations independent
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, bin);
-      if (bin >= 0 && (peers & lt_mask) == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
-      __syncwarp();
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -406,6 +423,8 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     }
     int base = incl - tot;
     if (bin == quad_bin) s_i[34] = base;  // first rank of the quad bins (bins <= quad_bin)
+    const unsigned used = __ballot_sync(0xffffffffu, tot > 0);
+    if (lane == 0) s_i[33] = __popc(used) <= 1;  // one bin: the rank order is the request order
     for (int w = 0; w < nw; ++w) {
       const int c = s_wcnt[w * kNumBins + bin];
       s_wcnt[w * kNumBins + bin] = base;
@@ -416,30 +435,38 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   // read before the barriers below: the scratch is the merge area, which consumers overwrite
   // once their first item is done
   const int quad_rank = s_i[34];
+  const bool one_bin = s_i[33] != 0;
   if (tid == 0) L4_MARK(8);
-  for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
-    const int b = t0 + lane;
-    int bin = -1, ns = 0;
-    if (b < r1) {
-      const int pg = pages_of(s_len[b]);
-      ns = nsplit_of(pg, C);
-      bin = bin_of(pg, ns);
+  if (one_bin) {  // fast path, same result: a stable sort of one bin is the identity
+    for (int b = tid; b < B; b += nthr) s_rb[b] = b | ((s_off[b] >> 16) << 16);
+  } else {
+    for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
+      const int b = t0 + lane;
+      int bin = -1, ns = 0;
+      if (b < r1) {
+        const int packed = s_off[b];                // pass 1's (bin, nsplit)
+        bin = packed & 0xffff;
+        ns = packed >> 16;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      const int lower = __popc(peers & lt_mask);
+      int pos = 0;
+      if (bin >= 0) pos = s_wcnt[warp * kNumBins + bin] + lower;
+      __syncwarp();
+      if (bin >= 0) {
+        s_rb[pos] = b | (ns << 16);  // b < 8192, ns <= kMaxSplits
+        if (lower == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
+      }
+      __syncwarp();
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    const int lower = __popc(peers & lt_mask);
-    int pos = 0;
-    if (bin >= 0) pos = s_wcnt[warp * kNumBins + bin] + lower;
-    __syncwarp();
-    if (bin >= 0) {
-      s_rb[pos] = b | (ns << 16);  // b < 8192, ns <= kMaxSplits
-      if (lower == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
-    }
-    __syncwarp();
   }
   __syncthreads();
   if (tid == 0) L4_MARK(9);
-  // ---- item offsets: exclusive scan of nsplit * Hkv in rank order (same warp ranges)
-  {
+  // ---- item offsets: exclusive scan of nsplit * Hkv in rank order (same warp ranges); with no
+  // split request (N = B * Hkv) it is r * Hkv (fast path, same result)
+  if (N == (long long)B * Hkv) {
+    for (int r = tid; r <= B; r += nthr) s_off[r] = r * Hkv;
+  } else {
     int wsum = 0;
     for (int t0 = r0; t0 < r1; t0 += 32) {
       const int r = t0 + lane;
@@ -480,16 +507,21 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
 // Work item `i` of the plan held in shared memory (fused path) — the same item plan_kernel
 // writes at index i: rank r = the last rank whose first item is <= i, then (kv head, split).
 __device__ __forceinline__ WorkItem item_from_plan(int i, int n, const int* s_len, const int* s_ptr,
-                                                   const int* s_rb, const int* s_off, int B, int C) {
+                                                   const int* s_rb, const int* s_off, int B, int Hkv) {
   WorkItem it;
   if (i >= n) {
     it.b = -1; it.h = 0; it.pbeg = 0; it.pend = 0; it.last_valid = 0; it.part_base = 0; it.nsplit = 1; it.split = 0;
     return it;
   }
-  int lo = 0, hi = B - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+  int lo = 0;
+  if (n == B * Hkv) {  // no split request: rank r owns items [r * Hkv, (r + 1) * Hkv)
+    lo = i / Hkv;
+  } else {
+    int hi = B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= i) lo = mid; else hi = mid - 1;
+    }
   }
   const int b = s_rb[lo] & 0xffff, ns = s_rb[lo] >> 16;
   const int L = s_len[b];
@@ -928,7 +960,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int W = gridDim.x;
   // producer lane 0: the first three scheduler tickets, in flight while the plan is built
   int raw_t0 = -1, raw_t1 = -1, raw_t2 = -1;
-  if (!early && !early_plan && warp == kConsumerWarps && lane == 0) {
+  if (kTicketAhead > 1 && !early && !early_plan && warp == kConsumerWarps && lane == 0) {
     raw_t0 = atomicAdd(&a.header->sched_next, 1);
     raw_t1 = atomicAdd(&a.header->sched_next, 1);
     raw_t2 = atomicAdd(&a.header->sched_next, 1);
@@ -952,7 +984,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   if (early_plan) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (warp == kConsumerWarps && lane == 0) {
+    if (kTicketAhead > 1 && warp == kConsumerWarps && lane == 0) {
       raw_t0 = atomicAdd(&a.header->sched_next, 1);
       raw_t1 = atomicAdd(&a.header->sched_next, 1);
       raw_t2 = atomicAdd(&a.header->sched_next, 1);
@@ -973,7 +1005,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (threadIdx.x == 0) L4_MARK(2);
   auto get_item = [&](int i) -> WorkItem {
     if constexpr (kFused)
-      return item_from_plan(i, n_items, p_len, p_ptr, p_rb, p_off, a.B, plan_C);
+      return item_from_plan(i, n_items, p_len, p_ptr, p_rb, p_off, a.B, a.Hkv);
     else
       return load_item(a.items, i, n_items);
   };
@@ -1048,6 +1080,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       if constexpr (kStages % kConsumerWarps != 0) st_release_cta(sbase + SL::seq + st * 4, (int)qseq);
       mbar_arrive(bar_full + st * 8);
     };
+    // Quad unit u (items f .. f + 3, one per consumer warp): lanes 0..3 look up one item each,
+    // lane 0 posts the slot and issues the Q rows (slot copies, or ring positions qbase + w at
+    // G = 8); page j of item w goes out as ring page qbase' + 4 j + w (null stages pad the
+    // shorter items), so warp w always owns the ring positions = w (mod 4) of the unit.
     // Quad unit u (items f .. f + 3, one per consumer warp): lanes 0..3 look up one item each,
     // lane 0 posts the slot and issues the Q rows (slot copies, or ring positions qbase + w at
     // G = 8); page j of item w goes out as ring page qbase' + 4 j + w (null stages pad the
@@ -1167,17 +1203,51 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     if (early) {  // from here on the scheduler state of the workspace is touched
       asm volatile("griddepcontrol.wait;" ::: "memory");
-      if (lane == 0) {
+      if (kTicketAhead > 1 && lane == 0) {
         raw_t0 = atomicAdd(&a.header->sched_next, 1);
         raw_t1 = atomicAdd(&a.header->sched_next, 1);
         raw_t2 = atomicAdd(&a.header->sched_next, 1);
       }
     }
+    uint32_t k = 0;
+    int raw_p = -1;
+    if constexpr (kTicketAhead == 1) {
+      // One unit at a time: the ticket for the next unit is drawn once this unit's pages are
+      // issued (the ring's kStages pages in flight cover the atomic's round trip), so no CTA
+      // holds work it has not started when the counter runs out: the launch ends balanced.
+      for (; i_cur < n_units; ++k) {
+        if (is_quad(i_cur)) {
+          if (!(k == 0 && first_done)) issue_quad(i_cur, k);
+        } else {
+          if (k > 0 && lane == 0) post_item(k, cur, unit_item(i_cur));
+          const int np = cur.pend - cur.pbeg;
+          const int jstart = k == 0 ? pre : 0;  // item 0's first `pre` pages went out above
+          if (jstart < np) {
+            int j0 = jstart & ~31;
+            int blk = j0 == 0 ? cur_idx : ((j0 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + lane) : 0);
+            for (; j0 < np; j0 += 32) {
+              const int nb = (j0 + 32 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + 32 + lane) : 0;
+              const int cnt = min(32, np - j0);
+              for (int j = max(jstart - j0, 0); j < cnt; ++j) {
+                const int page = __shfl_sync(0xffffffffu, blk, j);
+                if (lane == 0) issue_page(page, cur.h);
+                ++qseq;
+              }
+              blk = nb;
+            }
+          }
+        }
+        i_cur = resolve(issue());
+        if (i_cur < n_units) {
+          cur = get_item(unit_item(i_cur));
+          cur_idx = (!is_quad(i_cur) && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
+        }
+      }
+    } else {
     int i_nxt = resolve(raw_t0);
     WorkItem nxt = get_item(unit_item(i_nxt));
     int i_nn = resolve(raw_t1);
-    int raw_p = raw_t2;  // resolved in iteration 0
-    uint32_t k = 0;
+    raw_p = raw_t2;  // resolved in iteration 0
     for (; i_cur < n_units; ++k) {
       // prefetch: the next unit's first page ids, the unit after's first item, one more ticket
       const int nxt_idx = (i_nxt < n_units && !is_quad(i_nxt) && lane < nxt.pend - nxt.pbeg)
@@ -1222,6 +1292,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       i_nxt = i_nn;
       nxt = nn;
       i_nn = i_nnn;
+    }
     }
     // the last issued ticket must complete before this CTA reports done
     if (resolve(raw_p) != -7 && lane == 0) {
@@ -1383,6 +1454,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     const WorkItem it = s_items[slot].it[0];
     const int item_idx = s_items[slot].idx;
     if (it.b < 0) break;
+#ifdef L4_TRACE
+    if (ct == 0) {
+      g_trace_last[blockIdx.x * 4 + 0] = trace_now();
+      g_trace_last[blockIdx.x * 4 + 1] = (unsigned long long)(it.pend - it.pbeg);
+      g_trace_last[blockIdx.x * 4 + 2] = (unsigned long long)it.nsplit;
+      g_trace_last[blockIdx.x * 4 + 3] = (unsigned long long)item_idx;
+    }
+#endif
     uint32_t qf[8][2];
     {
       const unsigned char* qs = smem + SL::qslots + slot * SL::qslot_bytes;
@@ -1727,6 +1806,9 @@ extern "C" int l4_debug_cks(unsigned* host, int n, int clear) {
 #ifdef L4_TRACE
 extern "C" int l4_trace_read(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (size_t)n);
+}
+extern "C" int l4_trace_read_last(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace_last, sizeof(unsigned long long) * (size_t)n);
 }
 extern "C" int l4_trace_clear(void) {
   static unsigned long long zeros[4096 * 16];

@@ -55,12 +55,17 @@ def main():
                         flags=l4.L4_DECODE_EARLY_INPUTS)
     early = lambda: l4.attention_call(pe, wl.q, wl.k, wl.v, wl.indptr, wl.indices, wl.kv_len, wl.table.total_pages,
                                       wl.out, wl.lse, ws)
+    pp = l4.make_params(len(wl.lens), wl.shape.num_q_heads, wl.shape.num_kv_heads, chunk_pages=args.chunk,
+                        flags=getattr(l4, "L4_DECODE_EARLY_PLAN", 0))
+    eplan = lambda: l4.attention_call(pp, wl.q, wl.k, wl.v, wl.indptr, wl.indices, wl.kv_len, wl.table.total_pages,
+                                      wl.out, wl.lse, ws)
     plan()
     if args.quick:
-        t_fused, t_early = timeit(fused), timeit(early)
-        print(f"{args.workload} {args.bin or args.fig2 or args.uniform or ''} {os.environ.get('L4_LIB', 'libl4.so')}: fused {t_fused:.2f} us "
-              f"({wl.bytes_kv / (t_fused * 1e-6) / 1e9:.0f} GB/s), early {t_early:.2f} us "
-              f"({wl.bytes_kv / (t_early * 1e-6) / 1e9:.0f} GB/s)")
+        t_fused, t_eplan, t_early = timeit(fused), timeit(eplan), timeit(early)
+        gb = lambda t: wl.bytes_kv / (t * 1e-6) / 1e9
+        print(f"{args.workload} {args.bin or args.fig2 or args.uniform or ''} {os.environ.get('L4_LIB', 'libl4.so')}: "
+              f"plain {t_fused:.2f} us ({gb(t_fused):.0f} GB/s), early-plan {t_eplan:.2f} us ({gb(t_eplan):.0f}), "
+              f"early {t_early:.2f} us ({gb(t_early):.0f})")
         return
     t_plan = timeit(plan)
     t_run = timeit(run)

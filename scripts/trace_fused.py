@@ -70,6 +70,23 @@ def main():
           f"for ring slots {np.median(acc[:, 2]) / 1e3:.1f}; items {np.median(acc[:, 3]):.0f} "
           f"(min {acc[:, 3].min():.0f}, max {acc[:, 3].max():.0f}); consumer warp0 waiting for the next item "
           f"(Q) {np.median(acc2[:, 0]) / 1e3:.1f}; warp0 page compute {np.median(acc2[:, 1]) / 1e3:.1f}")
+    if hasattr(l4.lib(), "l4_trace_read_last"):
+        lb = (ctypes.c_ulonglong * (4096 * 4))()
+        l4.lib().l4_trace_read_last(lb, 4096 * 4)
+        last = np.frombuffer(lb, dtype=np.uint64).reshape(4096, 4)[:ncta].astype(np.float64)
+        ok = last[:, 0] > 0
+        if not ok.any():
+            ok = None
+    if hasattr(l4.lib(), "l4_trace_read_last") and ok is not None:
+        st = (last[ok, 0] - t0) / 1e3
+        done = rel[ok, 5]
+        print(f"  last CTA-wide item per CTA: start p10/p50/p90 {np.percentile(st, 10):.1f}/{np.median(st):.1f}/"
+              f"{np.percentile(st, 90):.1f} us, pages p50 {np.median(last[ok, 1]):.0f} max {last[ok, 1].max():.0f}, "
+              f"split {int((last[ok, 2] > 1).sum())}/{int(ok.sum())}; the 10 latest-finishing CTAs (done us, last "
+              f"start us, pages, splits):")
+        order = np.argsort(-done)[:10]
+        print("   ", [(round(float(done[i]), 1), round(float(st[i]), 1), int(last[ok][i, 1]), int(last[ok][i, 2]))
+                      for i in order])
     for k, name in enumerate(["entry", "pdl_wait", "plan", "tma0", "land0", "done", "p_load", "p_count", "p_pass1", "p_pass2"]):
         c = rel[:, k]
         c = c[(c > -1e6) & (c < 1e7)]  # marks a CTA never reached hold stale values

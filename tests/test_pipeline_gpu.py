@@ -201,14 +201,19 @@ def test_bidirectional_precopy_overlaps_next_decode():
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 rt, op = rts[r], ops[r]
+                kv_len, indptr = rt.device_batch()       # pre-copies leave the batch unchanged
+                B = len(kv_len)
+                d_len, d_ptr = (torch.from_numpy(x).cuda() for x in (kv_len, indptr))
+                torch.cuda.synchronize()
                 for step in range(2):
                     op.before_decode()
-                    kv_len, indptr = rt.device_batch()
-                    B = len(kv_len)
-                    d_len, d_ptr = (torch.from_numpy(x).cuda() for x in (kv_len, indptr))
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
-                    for _ in range(20):      # a long decode window
+                    # keep the device ahead of the host (as in a GPU-bound serving loop): the copy
+                    # enqueued by apply() starts when this step's decode ends, while the host has
+                    # long enqueued the next step's decode
+                    torch.cuda._sleep(20_000_000)
+                    for _ in range(4):
                         l4.decode_attention(q[:B], rt.pool["k"], rt.pool["v"], d_ptr, rt.table, d_len)
                     e1.record()
                     op.after_decode(e1, e0)
