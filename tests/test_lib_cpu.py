@@ -181,7 +181,7 @@ def test_decode_param_validation():
                        (dict(num_q_heads=48, num_kv_heads=3), l4.L4_ERR_UNSUPPORTED),
                        (dict(batch=-1), l4.L4_ERR_INVALID_ARG),
                        (dict(batch=8193), l4.L4_ERR_UNSUPPORTED),
-                       (dict(flags=2), l4.L4_ERR_INVALID_ARG),
+                       (dict(flags=4), l4.L4_ERR_INVALID_ARG),
                        (dict(out_dtype=7), l4.L4_ERR_INVALID_ARG),
                        (dict(sm_scale=float("nan")), l4.L4_ERR_INVALID_ARG)]:
         args = dict(batch=4, num_q_heads=8, num_kv_heads=2, head_dim=128, page_size=16)
