@@ -17,7 +17,7 @@
 //      l4_decode_run, e.g. for every layer of a step).
 //  a2  decode_kernel (persistent, 1 producer + 4 consumer warps per CTA,
 //      2 CTAs per SM): items are handed out dynamically (first one static,
-//      then atomic tickets issued one item ahead), so CTAs that finish early
+//      then one atomic ticket per unit), so CTAs that finish early
 //      take the next-largest item.  The producer warp streams each (page, kv
 //      head) K and V slice (4 KB each, HND layout) with one TMA each
 //      (cp.async.bulk.tensor, 128B swizzle, L2 evict-first) into an 8-stage
@@ -96,12 +96,6 @@ constexpr int kQuadTailPerCta = L4_QUAD_TAIL;  // CTA-wide items per CTA at the 
 #define L4_QUAD_MIN 4
 #endif
 constexpr int kQuadMinPerCta = L4_QUAD_MIN;  // quads only if there are at least this many per CTA
-#ifndef L4_TICKET_AHEAD
-#define L4_TICKET_AHEAD 3
-#endif
-// Scheduler tickets a CTA holds beyond its current unit: 3 (two resolved, one in flight; no
-// atomic round trip between units) or 1 (drawn when the current unit's pages are out).
-constexpr int kTicketAhead = L4_TICKET_AHEAD;
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kLog2e = 1.44269504088896340736f;
 
@@ -958,13 +952,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (threadIdx.x == 0) L4_MARK(1);
 
   const int W = gridDim.x;
-  // producer lane 0: the first three scheduler tickets, in flight while the plan is built
-  int raw_t0 = -1, raw_t1 = -1, raw_t2 = -1;
-  if (kTicketAhead > 1 && !early && !early_plan && warp == kConsumerWarps && lane == 0) {
-    raw_t0 = atomicAdd(&a.header->sched_next, 1);
-    raw_t1 = atomicAdd(&a.header->sched_next, 1);
-    raw_t2 = atomicAdd(&a.header->sched_next, 1);
-  }
   int n_items, plan_C = 0, n_wide, q_pages = 0;
   int *p_len = nullptr, *p_ptr = nullptr, *p_rb = nullptr, *p_off = nullptr;
   if constexpr (kFused) {
@@ -982,14 +969,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     n_wide = SL::quads ? a.header->n_wide : n_items;
     q_pages = a.header->quad_pages;
   }
-  if (early_plan) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (kTicketAhead > 1 && warp == kConsumerWarps && lane == 0) {
-      raw_t0 = atomicAdd(&a.header->sched_next, 1);
-      raw_t1 = atomicAdd(&a.header->sched_next, 1);
-      raw_t2 = atomicAdd(&a.header->sched_next, 1);
-    }
-  }
+  if (early_plan) asm volatile("griddepcontrol.wait;" ::: "memory");
   // Scheduling units: items [0, n_wide) one per unit (CTA-wide); then the quad-eligible suffix
   // four items per unit (one per consumer warp), except its last kQuadTailPerCta x W items,
   // which run CTA-wide again so the end of the launch has the fine granularity of single
@@ -1021,12 +1001,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 #endif
     const uint64_t policy = policy_evict_first();
     bool exhausted = false;
-    // Dynamic LPT scheduling: the first item is blockIdx.x, later ones come from an atomic
-    // ticket (W + ticket) so idle CTAs take the next-largest item.  Tickets are issued one
-    // item ahead of their use (three were issued before the plan was built), so no atomic
-    // round trip sits between two items or in front of the first TMA.  Every issued ticket
-    // is resolved (its value consumed) before this CTA reports done: the last CTA to report
-    // resets the scheduler for the next run.
+    // Dynamic LPT scheduling: the first unit is blockIdx.x, later ones come from an atomic
+    // ticket (W + ticket) drawn when the current unit's pages are issued, so idle CTAs take the
+    // next-largest unit and no CTA holds work it has not started when the counter runs out
+    // (round 1 held three tickets ahead: C3 ended over an 80 us spread of CTA finish times).
+    // The atomic's round trip is covered by the kStages pages the ring still holds.  Every
+    // drawn ticket is resolved before this CTA reports done: the last CTA to report resets
+    // the scheduler for the next run.
     auto resolve = [&](int raw) -> int {
       const int t = __shfl_sync(0xffffffffu, raw, 0);
       if (t < 0 || exhausted) return n_units;
@@ -1201,17 +1182,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         blk = nb;
       }
     }
-    if (early) {  // from here on the scheduler state of the workspace is touched
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      if (kTicketAhead > 1 && lane == 0) {
-        raw_t0 = atomicAdd(&a.header->sched_next, 1);
-        raw_t1 = atomicAdd(&a.header->sched_next, 1);
-        raw_t2 = atomicAdd(&a.header->sched_next, 1);
-      }
-    }
+    // from here on the scheduler state of the workspace is touched
+    if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t k = 0;
-    int raw_p = -1;
-    if constexpr (kTicketAhead == 1) {
+    {
       // One unit at a time: the ticket for the next unit is drawn once this unit's pages are
       // issued (the ring's kStages pages in flight cover the atomic's round trip), so no CTA
       // holds work it has not started when the counter runs out: the launch ends balanced.
@@ -1243,59 +1217,9 @@ __global__ void __launch_bounds__(kThreads, 2)
           cur_idx = (!is_quad(i_cur) && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
         }
       }
-    } else {
-    int i_nxt = resolve(raw_t0);
-    WorkItem nxt = get_item(unit_item(i_nxt));
-    int i_nn = resolve(raw_t1);
-    raw_p = raw_t2;  // resolved in iteration 0
-    for (; i_cur < n_units; ++k) {
-      // prefetch: the next unit's first page ids, the unit after's first item, one more ticket
-      const int nxt_idx = (i_nxt < n_units && !is_quad(i_nxt) && lane < nxt.pend - nxt.pbeg)
-                              ? __ldg(a.indices + nxt.pbeg + lane) : 0;
-      const WorkItem nn = get_item(unit_item(i_nn));
-      const int i_nnn = resolve(raw_p);  // issued one iteration ago
-      raw_p = issue();
-      if (is_quad(i_cur)) {
-        if (!(k == 0 && first_done)) issue_quad(i_cur, k);
-        i_cur = i_nxt;
-        cur = nxt;
-        cur_idx = nxt_idx;
-        i_nxt = i_nn;
-        nxt = nn;
-        i_nn = i_nnn;
-        continue;
-      }
-      if (k > 0 && lane == 0) post_item(k, cur, unit_item(i_cur));
-      const int np = cur.pend - cur.pbeg;
-      const int jstart = k == 0 ? pre : 0;  // item 0's first `pre` pages went out above
-      if (jstart < np) {
-        int j0 = jstart & ~31;
-        int blk = j0 == 0 ? cur_idx : ((j0 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + lane) : 0);
-        for (; j0 < np; j0 += 32) {
-          const int nb = (j0 + 32 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + 32 + lane) : 0;
-          const int cnt = min(32, np - j0);
-          for (int j = max(jstart - j0, 0); j < cnt; ++j) {
-            const int page = __shfl_sync(0xffffffffu, blk, j);
-            if (lane == 0) issue_page(page, cur.h);
-#ifdef L4_DEBUG_CKS
-            if (lane == 0 && unit_item(i_cur) < 16384)
-              atomicAdd(&g_cks[unit_item(i_cur) * 4 + 3], (unsigned)page * (unsigned)(j0 + j + 1));
-#endif
-            ++qseq;
-          }
-          blk = nb;
-        }
-      }
-      i_cur = i_nxt;
-      cur = nxt;
-      cur_idx = nxt_idx;
-      i_nxt = i_nn;
-      nxt = nn;
-      i_nn = i_nnn;
     }
-    }
-    // the last issued ticket must complete before this CTA reports done
-    if (resolve(raw_p) != -7 && lane == 0) {
+    // every ticket this CTA drew has been resolved: report done
+    if (lane == 0) {
       const int done = atomicAdd(&a.header->sched_done, 1);
       if (done == W - 1) {  // every CTA stopped drawing: reset for the next run
         a.header->sched_next = 0;
