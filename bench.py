@@ -531,7 +531,7 @@ def extra_lines(steps: int, warmup: int, peak: float):
                   (synth.SHAPE_LLAMA3_70B, 200)):
         w = Workload(f"short{L}", np.full(1024, L, dtype=np.int64), sh, copies=4)
         key = f"short{'70b_' if sh.num_q_heads == 64 else ''}{L}"
-        e = both(key, w, "short200" if key == "short200" else None)
+        e = both(key, w, key if key in ("short64", "short200") else None)
         short.append([sh.name, L, round(e["ms"] * 1e3, 2), e["kv_gbs"], round(e["cold_ms"] * 1e3, 2)])
         del w
         torch.cuda.empty_cache()

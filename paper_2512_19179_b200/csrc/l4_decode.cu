@@ -70,7 +70,7 @@ constexpr int kCombineGroup = 16;                     // two-level combine: spli
 constexpr int kMaxCombine = kMaxSplits / kCombineGroup;  // partials read by one combine (>= group)
 constexpr int kMinChunk = 8;                          // pages
 #ifndef L4_ITEMS_PER_CTA
-#define L4_ITEMS_PER_CTA 6
+#define L4_ITEMS_PER_CTA 8
 #endif
 constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
