@@ -216,7 +216,7 @@ def _full_size(lens, shape, seed):
     kl = torch.from_numpy(table.kv_len).cuda()
     out, lse = l4.decode_attention(q, k, v, ip, ix, kl)
     torch.cuda.synchronize()
-    for flags in (0, l4.L4_DECODE_EARLY_INPUTS):
+    for flags in (0, l4.L4_DECODE_EARLY_PLAN, l4.L4_DECODE_EARLY_INPUTS):
         params = l4.make_params(B, shape.num_q_heads, shape.num_kv_heads, flags=flags)
         ws = l4.alloc_workspace(params, table.total_pages)
         l4.poison_partials(params, ws)
@@ -318,10 +318,12 @@ def test_fused_equals_plan_plus_run_bitwise(G, chunk):
     o3, l3 = _fused(params, table, qd, kd, vd, ip, ix, kl, ws)   # repeat: self-cleaning state
     pe = l4.make_params(table.batch, Hkv * G, Hkv, chunk_pages=chunk, flags=l4.L4_DECODE_EARLY_INPUTS)
     early = [_fused(pe, table, qd, kd, vd, ip, ix, kl, ws) for _ in range(3)]  # back to back (PDL overlap)
+    pp = l4.make_params(table.batch, Hkv * G, Hkv, chunk_pages=chunk, flags=l4.L4_DECODE_EARLY_PLAN)
+    eplan = [_fused(pp, table, qd, kd, vd, ip, ix, kl, ws) for _ in range(3)]  # plan under the previous tail
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
     assert torch.equal(o2, o3) and torch.equal(l2, l3)
-    for o4, l4_ in early:
+    for o4, l4_ in early + eplan:
         assert torch.equal(o2, o4) and torch.equal(l2, l4_)
     _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
 

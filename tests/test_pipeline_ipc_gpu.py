@@ -52,6 +52,7 @@ def _worker(rank, world, port, steps, lead, out_q):
             before = {rid: len(p) for rid, p in rt.pages.items()}
             ev = sim.step()
             rt.apply(ev, dist)
+            rt.ops.before_decode()   # this stream waits for the senders' pushes (their IPC events)
             migrated_in = {m[0] for m in ev.migrations if m[2] == rank}
             for rid, pages in rt.pages.items():
                 if rid in migrated_in:
@@ -66,7 +67,8 @@ def _worker(rank, world, port, steps, lead, out_q):
             t.cuda.synchronize()
             dist.barrier()   # tags written before any peer pushes these pages on
             used = sum(len(p) for p in rt.pages.values()) + sum(len(p) for p in rt.incoming.values())
-            assert pool["alloc"].num_free() == pool["alloc"].num_pages - used
+            pending = sum(len(p) for _, p in pool["pending"])   # freed, waiting for their last reader
+            assert pool["alloc"].num_free() + pending == pool["alloc"].num_pages - used, "page accounting"
         fps = [None] * world
         dist.all_gather_object(fps, sim.fingerprint())
         rt.ops.close_ipc()
