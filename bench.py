@@ -893,13 +893,13 @@ def pipeline_line(args, world, rank, local):
     clocks = ClockSampler(local)
     clocks.start()
     clk = None
-    arms = (("l4", stages, True, 10), ("l4_static", stages, True, 0), ("round_robin", rr, False, 0),
-            ("l4_e2e", stages, True, 10))
+    arms = (("l4", stages, True, 0), ("l4_refined", stages, True, 10), ("round_robin", rr, False, 0),
+            ("l4_e2e", stages, True, 0))
     for name, st, l4arm, refine in arms:
-        # L4 arm: bid-ask receivers + intra-stage rebalancing, live (two-round)
-        # migration with an 8-token pre-copy lead, boundary refinement every 10 steps
-        # (P:369-379); l4_static: the same without refinement; baseline: one length-agnostic
-        # stage, round-robin placement
+        # L4 arm (the value): l4_partition's stages, bid-ask receivers + intra-stage rebalancing
+        # (P:391-399), live (two-round) migration with an 8-token pre-copy lead;
+        # l4_refined: the same with boundary refinement every 10 steps (NEXT#2);
+        # baseline: one length-agnostic stage, round-robin placement
         t = run_pipeline_arm(st, args.steps, args.warmup, rank, world, device,
                              precopy_lead=8 if l4arm else 0, policy="bidask" if l4arm else "round_robin",
                              rebalance_every=10 if l4arm else 0, e2e=name == "l4_e2e", refine_every=refine,
