@@ -2,6 +2,8 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "l4_internal.h"
 
 namespace l4 {
@@ -16,6 +18,9 @@ void set_error(const char* fmt, ...) {
 }
 
 void clear_error() { g_last_error[0] = '\0'; }
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 }  // namespace l4
 

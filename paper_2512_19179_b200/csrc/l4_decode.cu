@@ -1913,6 +1913,7 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
 
 extern "C" l4_status l4_decode_plan(const l4_decode_params* p, const int32_t* kv_len, const int32_t* page_indptr,
                                     int64_t total_pages, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx("l4_decode_plan");
   if (p && p->batch == 0) {
     int G = 0;
     return check_params(p, &G);
@@ -1923,6 +1924,7 @@ extern "C" l4_status l4_decode_plan(const l4_decode_params* p, const int32_t* kv
 extern "C" l4_status l4_decode_run(const l4_decode_params* p, const void* q, const void* k_pages, const void* v_pages,
                                    int64_t num_pages, const int32_t* page_indices, void* out, float* lse,
                                    void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx("l4_decode_run");
   return run_impl(p, q, k_pages, v_pages, num_pages, page_indices, out, lse, workspace, workspace_bytes,
                   static_cast<cudaStream_t>(stream));
 }
@@ -1932,6 +1934,7 @@ extern "C" l4_status l4_decode_attention(const l4_decode_params* p, const void* 
                                          const int32_t* page_indices, int64_t total_pages, const int32_t* kv_len,
                                          void* out, float* lse, void* workspace, size_t workspace_bytes,
                                          void* stream) {
+  NvtxRange nvtx("l4_decode_attention");
   // One launch: every CTA of the decode kernel plans in its own shared memory (B <= 1024).
   // Larger batches: the materialised plan (planner kernel) followed by the run.
   int G = 0;

@@ -18,6 +18,13 @@ inline l4_status fail(l4_status s, const char* msg) {
   return s;
 }
 
+// NVTX range for the duration of a C-ABI call (tracing): header-only NVTX v3, a few
+// ns when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+};
+
 }  // namespace l4
 
 #define L4_CHECK_ARG(cond, msg)                              \

@@ -156,6 +156,7 @@ using namespace l4;
 
 extern "C" l4_status l4_copy_pages(const l4_kv_view* src, const int32_t* src_pages, const l4_kv_view* dst,
                                    const int32_t* dst_pages, int64_t n_pages, void* stream) {
+  NvtxRange nvtx("l4_copy_pages");
   l4_status s = check_view(src, "src");
   if (s != L4_OK) return s;
   s = check_view(dst, "dst");
@@ -174,6 +175,7 @@ extern "C" l4_status l4_copy_pages(const l4_kv_view* src, const int32_t* src_pag
 extern "C" l4_status l4_migrate(const l4_kv_view* src, const int32_t* src_pages, int64_t n_pages,
                                 const l4_kv_view* dst, l4_page_pool* dst_pool, int32_t* dst_pages_out, void* stream,
                                 void* done_event) {
+  NvtxRange nvtx("l4_migrate");
   l4_status s = check_view(src, "src");
   if (s != L4_OK) return s;
   s = check_view(dst, "dst");

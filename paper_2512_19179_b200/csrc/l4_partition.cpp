@@ -296,6 +296,7 @@ class Partitioner {
 
 extern "C" l4_status l4_partition(const l4_partition_params* p, const int64_t* input_len, const int64_t* output_len,
                                   int64_t n, l4_stage* stages_out, int32_t* num_stages_out, double* objective_out) {
+  l4::NvtxRange nvtx("l4_partition");
   L4_CHECK_ARG(p != nullptr, "l4_partition: params is NULL");
   L4_CHECK_ARG(stages_out && num_stages_out && objective_out, "l4_partition: output pointer is NULL");
   L4_CHECK_ARG(n >= 0, "l4_partition: n < 0");

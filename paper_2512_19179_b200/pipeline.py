@@ -526,6 +526,16 @@ class RankRuntime:
     def apply(self, ev: StepEvents, comm):
         """Apply one step's events to this rank: retire, grow page lists (new tokens),
         migrate KV pages out/in (P2P), admit new requests."""
+        nvtx = getattr(getattr(getattr(self.ops, "torch", None), "cuda", None), "nvtx", None)
+        if nvtx is not None:
+            nvtx.range_push("l4.pipeline.apply")
+        try:
+            self._apply(ev, comm)
+        finally:
+            if nvtx is not None:
+                nvtx.range_pop()
+
+    def _apply(self, ev: StepEvents, comm):
         me = self.rank
         free_sent = getattr(self.ops, "free_after_transfer", self.ops.free)
         for rid, r in ev.retired:
