@@ -304,7 +304,7 @@ constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWa
 __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict__ indptr, int B, int Hkv,
                           int num_ctas, int forced_chunk, int items_cap, int* s_len, int* s_ptr, int* s_rb,
                           int* s_off, unsigned char* scratch, int* C_out, int* N_out, int* Pmax_out,
-                          int quad_bin, int* Wide_out, int* QPages_out) {
+                          int quad_bin, int* Wide_out, int* QPages_out, int* TailChunk_out = nullptr) {
   long long* s_ll = reinterpret_cast<long long*>(scratch);
   int* s_i = reinterpret_cast<int*>(scratch + 32 * 8);
   unsigned* s_u = reinterpret_cast<unsigned*>(scratch + 32 * 8 + 36 * 4);
@@ -488,6 +488,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     if (tid == 0) s_off[B] = (int)N;
   }
   __syncthreads();
+  if (TailChunk_out) *TailChunk_out = 0;  // no guided tail (DESIGN §4.2 negative results)
   *C_out = C;
   *N_out = (int)N;
   *Pmax_out = Pmax;
@@ -548,9 +549,9 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
   int* s_rb = s_ptr + Bs;
   int* s_off = s_rb + Bs;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  int C, N, Pmax, Nw, Qb;
+  int C, N, Pmax, Nw, Qb, Ct;
   plan_core(a.kv_len, a.indptr, a.B, a.Hkv, a.num_ctas, a.forced_chunk, a.items_cap, s_len, s_ptr, s_rb, s_off,
-            scratch, &C, &N, &Pmax, a.quad_bin, &Nw, &Qb);
+            scratch, &C, &N, &Pmax, a.quad_bin, &Nw, &Qb, &Ct);
   // ---- items: one thread per (request rank, kv head) writes that pair's splits
   for (int x = tid; x < a.B * a.Hkv; x += nthr) {
     const int r = x / a.Hkv, h = x - r * a.Hkv;
@@ -582,6 +583,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) plan_kernel(PlanArgs a) {
     hd.items_cap = a.items_cap;
     hd.n_wide = Nw;
     hd.quad_pages = Qb;
+    hd.tail_chunk = Ct;  // guided tail chunk (0: none)
     hd.sched_next = 0;
     hd.sched_done = 0;
     *a.header = hd;

@@ -163,10 +163,11 @@ def test_plan_covers_every_token_once():
             sizes.append(0 if npg == 0 else -(-npg // plain_ns))
             if plain_ns > 1:  # the quad-bin bound: a split request's largest split exceeds 2C/3
                 assert 3 * sizes[-1] > 2 * C
-            # requests of <= 2C pages are split only in the guided tail, into tail chunks
+            # only the guided tail (automatic chunk) splits differently: split requests whose work
+            # starts in the plan's tail get pieces of the tail chunk (at most 512)
             if ns != plain_ns:
                 Ct = info.tail_chunk_pages
-                assert chunk == 0 and Ct > 0 and ns == -(-npg // Ct) and ns > plain_ns
+                assert chunk == 0 and Ct > 0 and plain_ns > 1 and ns == min(512, -(-npg // Ct)) and ns > plain_ns
         expect = sum(8 * ((int(L) + 15) // 16) for L in table.kv_len)
         assert len(covered) == expect
         # length-binned, longest bin first: bins are non-increasing along the work list
