@@ -668,6 +668,10 @@ def single_gpu_line(args, rank, world, local):
                    "plan": {"items": info.num_items, "chunk_pages": info.chunk_pages, "ctas": info.num_ctas},
                    "call": "l4_decode_attention, plain (no early-input overlap), back-to-back steps"},
         "tokens_per_s": round(world * len(wl.lens) / (ms / 1e3), 1),
+        "tokens_per_s_depth_normalised": {
+            "value": round(world * len(wl.lens) / (ms / 1e3) / (80 if wl.shape.num_q_heads == 64 else 32), 1),
+            "layers": 80 if wl.shape.num_q_heads == 64 else 32,
+            "note": "SURVEY 8(d): B / (n_layers x t_call), attention time only (Llama-3-8B 32 / -70B 80 layers)"},
         "pct_hbm_peak": round(100.0 * value / (world * peak), 2),
         "gpu_launches": args.steps * (1 if len(wl.lens) <= 1024 else 2),
         "clocks": clk,

@@ -252,6 +252,19 @@ def test_full_size_c3():
     _full_size(synth.lengths_c3(0), synth.SHAPE_LLAMA3_8B, 0)
 
 
+def test_full_size_fig2_mixed():
+    """Fig. 2 (`fig:interference`) analogue at full size: batch 512, 32 requests of 50,000 tokens
+    among 1,000-token ones — long split requests and many short unsplit ones in one launch."""
+    _full_size(synth.lengths_fig2(512, 32, 1000, 50000), synth.SHAPE_LLAMA3_8B, 3)
+
+
+def test_full_size_long_stage():
+    """A long-stage batch (12 requests around 84K tokens, C3's [64K, 128K) class refilled):
+    every request split tens of ways, two-level combines."""
+    lens = np.random.default_rng(12).integers(70000, 100001, size=12)
+    _full_size(lens, synth.SHAPE_LLAMA3_8B, 4)
+
+
 def test_full_size_c4():
     _full_size(synth.lengths_c4(0), synth.SHAPE_LLAMA3_70B, 0)
 
