@@ -1,5 +1,6 @@
 """compute-sanitizer over the library's kernels: memcheck (out-of-bounds / misaligned
-accesses), racecheck (shared-memory hazards), synccheck (barrier misuse)."""
+accesses), racecheck (shared-memory hazards), synccheck (barrier misuse), initcheck (reads of
+uninitialised device memory)."""
 import os
 import shutil
 import subprocess
@@ -12,7 +13,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_compute_sanitizer(tool):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
