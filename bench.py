@@ -897,6 +897,23 @@ def pipeline_line(args, world, rank, local):
             w.wait()
     torch.cuda.synchronize()
     dist.barrier()
+    # context: the same GPUs as independent replicas of the single-GPU C3 step (no pipeline, no
+    # migration; what length-agnostic data parallelism over N instances moves), max over ranks
+    rep = None
+    try:
+        spec = WORKLOADS["c3"]
+        wlr = Workload("c3", spec["lens"](), spec["shape"], seed=rank, copies=2)
+        steady_ms(wlr, 2, 3)
+        dist.barrier()
+        t_rep = torch.tensor([steady_ms(wlr, args.steps, args.warmup)], dtype=torch.float64, device=cdev)
+        dist.all_reduce(t_rep, op=dist.ReduceOp.MAX)
+        rep = {"kv_gbs": round(world * wlr.bytes_kv / (float(t_rep[0]) / 1e3) / 1e9, 1),
+               "ms_per_step": round(float(t_rep[0]), 5),
+               "note": "every rank runs the C3 single-GPU step on its own copy (plain calls); aggregate KV GB/s"}
+        del wlr
+        torch.cuda.empty_cache()
+    except Exception as e:  # noqa: BLE001 - context only
+        print(f"bench.py: replicas context failed: {e!r}"[:300], file=sys.stderr, flush=True)
     clocks = ClockSampler(local)
     clocks.start()
     clk = None
@@ -962,6 +979,7 @@ def pipeline_line(args, world, rank, local):
         "gpu_launches": int(l4r["launches"]),
         "clocks": clk,
         "nvlink": nvl,
+        "c3_replicas": rep,
         "pipeline": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                      for k, v in res.items()},
     }
