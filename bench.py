@@ -63,6 +63,27 @@ WORKLOADS = {
     "short200": dict(desc="B = 1024 x 200 tokens, Llama-3-8B shape (short-stage batch)", shape=synth.SHAPE_LLAMA3_8B,
                      lens=lambda: np.full(1024, 200, dtype=np.int64)),
 }
+
+
+def _stage_lengths(lo: int, hi: int):
+    """C3's length class [lo, hi) refilled: a homogeneous batch of the class's median length with
+    about C3's KV volume (<= 1024 requests) — the batch an L4 stage instance sees."""
+    lens = synth.lengths_c3(0)
+    sel = lens[(lens >= lo) & (lens < hi)]
+    L = int(np.median(sel))
+    return np.full(int(min(1024, max(1, round(lens.sum() / L)))), L, dtype=np.int64)
+
+
+STAGE_EDGES = [0, 1024, 4096, 16384, 65536, 1 << 30]
+for _lo, _hi in zip(STAGE_EDGES, STAGE_EDGES[1:]):
+    WORKLOADS[f"stage{_lo}"] = dict(desc=f"C3 length class [{_lo}, {_hi}) refilled (stage-shaped binned batch)",
+                                    shape=synth.SHAPE_LLAMA3_8B, lens=(lambda lo=_lo, hi=_hi: _stage_lengths(lo, hi)))
+for _L in (530,):
+    WORKLOADS[f"short{_L}"] = dict(desc=f"B = 1024 x {_L} tokens, Llama-3-8B shape", shape=synth.SHAPE_LLAMA3_8B,
+                                   lens=(lambda L=_L: np.full(1024, L, dtype=np.int64)))
+for _L in (64, 200):
+    WORKLOADS[f"short70b_{_L}"] = dict(desc=f"B = 1024 x {_L} tokens, Llama-3-70B shape", shape=synth.SHAPE_LLAMA3_70B,
+                                       lens=(lambda L=_L: np.full(1024, L, dtype=np.int64)))
 METRIC = "decode-attn KV GB/s (% HBM peak), mixed vs binned; tokens/s at 1/2/4/8 GPUs"
 L2_BYTES = 126 * (1 << 20)
 
@@ -515,14 +536,12 @@ def extra_lines(steps: int, warmup: int, peak: float):
                                       "bins_lo_batch_gbs": bins}
     stage = []
     for lo, hi in zip(edges, edges[1:]):
-        sel = lens[(lens >= lo) & (lens < hi)]
-        if len(sel) == 0:
+        if not ((lens >= lo) & (lens < hi)).any():
             continue
-        L = int(np.median(sel))
-        n = int(min(1024, max(1, round(lens.sum() / L))))
-        w = Workload(f"stage[{lo}]", np.full(n, L, dtype=np.int64), shape, copies=2)
-        e = both(f"stage{lo}", w)
-        stage.append([lo, L, n, e["kv_gbs"]])
+        sl = _stage_lengths(lo, hi)
+        w = Workload(f"stage[{lo}]", sl, shape, copies=2)
+        e = both(f"stage{lo}", w, f"stage{lo}")
+        stage.append([lo, int(sl[0]), len(sl), e["kv_gbs"]])
         del w
         torch.cuda.empty_cache()
     res["c3_stage_shaped_binned"] = stage
@@ -531,7 +550,7 @@ def extra_lines(steps: int, warmup: int, peak: float):
                   (synth.SHAPE_LLAMA3_70B, 200)):
         w = Workload(f"short{L}", np.full(1024, L, dtype=np.int64), sh, copies=4)
         key = f"short{'70b_' if sh.num_q_heads == 64 else ''}{L}"
-        e = both(key, w, key if key in ("short64", "short200") else None)
+        e = both(key, w, key)
         short.append([sh.name, L, round(e["ms"] * 1e3, 2), e["kv_gbs"], round(e["cold_ms"] * 1e3, 2)])
         del w
         torch.cuda.empty_cache()
@@ -1073,7 +1092,7 @@ def main(argv=None):
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c4", "short64", "short200"])
+    ap.add_argument("--workload", default="c3", choices=sorted(k for k in WORKLOADS if k != "c1"))
     ap.add_argument("--impl", default="l4", choices=["l4", "reference"])
     ap.add_argument("--copies", type=int, default=4, help="rotating input copies (L2 rotation)")
     ap.add_argument("--no-extra", action="store_true", help="skip the extra lines (C4, C2, binned, short, fig2)")
