@@ -1134,11 +1134,14 @@ def main(argv=None):
         line = pipeline_line(args, world, rank, local)
     else:
         line = single_gpu_line(args, rank, world, local)
-    if rank == 0 and line is not None:
-        print(json.dumps(line), flush=True)
     if world > 1 or pipe:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+        if world > 1:
+            time.sleep(1.0)  # let the other ranks' NCCL teardown log lines land before the JSON line
+    if rank == 0 and line is not None:
+        sys.stdout.flush()
+        print(json.dumps(line), flush=True)  # the last line of stdout
     return 0
 
 
