@@ -109,10 +109,20 @@ static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
 // every CTA, built only into trace variants (scripts/build_variant.sh ... -DL4_TRACE).
 __device__ unsigned long long g_trace[4096 * 16];
 __device__ unsigned long long g_trace_last[4096 * 4];  // last CTA-wide item: start, pages, splits, index
+__device__ long long g_trace_clk0[4096];  // clock64 at mark 0 (marks > 0: cycle-exact offsets from it)
 __device__ __forceinline__ void trace_mark(int k) {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  g_trace[blockIdx.x * 16 + k] = t;
+  if (k == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));  // 256 ns granularity on this part
+    g_trace[blockIdx.x * 16] = t;
+    g_trace_clk0[blockIdx.x] = clock64();
+  } else {  // globaltimer of mark 0 + elapsed SM cycles at L4_TRACE_MHZ (the clock under load)
+#ifndef L4_TRACE_MHZ
+#define L4_TRACE_MHZ 1965
+#endif
+    const long long dc = clock64() - *(volatile long long*)&g_trace_clk0[blockIdx.x];
+    g_trace[blockIdx.x * 16 + k] = *(volatile unsigned long long*)&g_trace[blockIdx.x * 16] + dc * 1000 / L4_TRACE_MHZ;
+  }
 }
 #define L4_MARK(k) trace_mark(k)
 __device__ __forceinline__ unsigned long long trace_now() {
@@ -244,6 +254,7 @@ struct PlanArgs {
 };
 
 constexpr int kPlanMaxWarps = kPlanThreads / 32;
+constexpr int kPlanUnroll = 8;  // request tiles per warp whose shared loads the planner issues together
 
 // Block-wide (sum int64, max int, or bits) in one pass.
 __device__ void block_reduce3(long long v, int m, unsigned bits, long long* s_ll, int* s_i, unsigned* s_u,
@@ -320,7 +331,37 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   {
     long long sum = 0;
     int mx = 0;
-    for (int b0 = tid; b0 < B; b0 += 4 * nthr) {  // four loads of each array in flight per thread
+    auto take = [&](int b, int Lv, int Pv) {
+      s_len[b] = Lv;
+      s_ptr[b] = Pv;
+      const int pg = pages_of(Lv);
+      sum += pg;
+      mx = max(mx, pg);
+    };
+    // one round of loads: 16-byte vectors of both arrays (B <= 1024 needs <= 2 per thread at
+    // 160 threads), scalars for the ragged tail or unaligned arrays
+    const bool vec = ((reinterpret_cast<uintptr_t>(kv_len) | reinterpret_cast<uintptr_t>(indptr)) & 15u) == 0;
+    const int B4 = vec ? (B >> 2) : 0;
+    for (int v0 = tid; v0 < B4; v0 += 2 * nthr) {
+      int4 Lv[2], Pv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int v = v0 + u * nthr;
+        Lv[u] = v < B4 ? reinterpret_cast<const int4*>(kv_len)[v] : make_int4(0, 0, 0, 0);
+        Pv[u] = v < B4 ? reinterpret_cast<const int4*>(indptr)[v] : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int v = v0 + u * nthr;
+        if (v < B4) {
+          take(4 * v, Lv[u].x, Pv[u].x);
+          take(4 * v + 1, Lv[u].y, Pv[u].y);
+          take(4 * v + 2, Lv[u].z, Pv[u].z);
+          take(4 * v + 3, Lv[u].w, Pv[u].w);
+        }
+      }
+    }
+    for (int b0 = 4 * B4 + tid; b0 < B; b0 += 4 * nthr) {  // four loads of each array in flight
       int Lv[4], Pv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -331,13 +372,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int b = b0 + u * nthr;
-        if (b < B) {
-          s_len[b] = Lv[u];
-          s_ptr[b] = Pv[u];
-          const int pg = pages_of(Lv[u]);
-          sum += pg;
-          mx = max(mx, pg);
-        }
+        if (b < B) take(b, Lv[u], Pv[u]);
       }
     }
     for (int x = tid; x < nw * kNumBins; x += nthr) s_wcnt[x] = 0;
@@ -352,7 +387,10 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     Cl = INT_MAX / 4;
   } else {
     const long long denom = (long long)num_ctas * kItemsPerCta;
-    Cl = max((long long)kMinChunk, (T * Hkv + denom - 1) / denom);
+    const long long num = T * Hkv + denom - 1;
+    // 32-bit division when it fits (a 64-bit one is a long software sequence on the critical path)
+    const long long q = num < (1ll << 31) ? (long long)((unsigned)num / (unsigned)denom) : num / denom;
+    Cl = max((long long)kMinChunk, q);
   }
   Cl = max(Cl, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
   int C = (int)min(Cl, (long long)(INT_MAX / 4));
@@ -366,16 +404,33 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   int min_split_bin;
   for (;;) {
     int wsum = 0, wms = kNumBins;
-    for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 1: per-warp bin histogram + item count
-      const int b = t0 + lane;
-      if (b < r1) {
-        const int pg = pages_of(s_len[b]);
-        const int ns = nsplit_of(pg, C);
-        const int bin = bin_of(pg, ns);
-        wsum += ns;
-        if (ns > 1) wms = min(wms, bin);
-        s_off[b] = bin | (ns << 16);              // kept for pass 2 (s_off is free until the scan)
-        atomicAdd(&s_wcnt[warp * kNumBins + bin], 1);  // counts only: iterations independent
+    // pass 1: per-warp bin histogram + item count, 8 tiles at a time with their loads issued
+    // together (a tile-by-tile loop serialised each shared load behind the previous tile's
+    // stores and atomics: ~0.2 us per tile at B = 1024)
+    for (int t0 = r0; t0 < r1; t0 += kPlanUnroll * 32) {
+      int Lr[kPlanUnroll];
+#pragma unroll
+      for (int i = 0; i < kPlanUnroll; ++i) {
+        const int b = t0 + i * 32 + lane;
+        Lr[i] = b < r1 ? s_len[b] : 0;
+      }
+#pragma unroll
+      for (int i = 0; i < kPlanUnroll; ++i) {
+        if (t0 + i * 32 >= r1) break;  // warp-uniform
+        const int b = t0 + i * 32 + lane;
+        int bin = -1;
+        if (b < r1) {
+          const int pg = pages_of(Lr[i]);
+          const int ns = nsplit_of(pg, C);
+          bin = bin_of(pg, ns);
+          wsum += ns;
+          if (ns > 1) wms = min(wms, bin);
+          s_off[b] = bin | (ns << 16);  // kept for pass 2 (s_off is free until the scan)
+        }
+        // one shared atomic per distinct bin of the tile (counts only: tiles independent); a
+        // lane-per-lane atomic serialises 32 ways on a homogeneous batch
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (bin >= 0 && (peers & lt_mask) == 0) atomicAdd(&s_wcnt[warp * kNumBins + bin], __popc(peers));
       }
     }
 #pragma unroll
@@ -432,26 +487,40 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   const bool one_bin = s_i[33] != 0;
   if (tid == 0) L4_MARK(8);
   if (one_bin) {  // fast path, same result: a stable sort of one bin is the identity
-    for (int b = tid; b < B; b += nthr) s_rb[b] = b | ((s_off[b] >> 16) << 16);
+    for (int b0 = tid; b0 < B; b0 += kPlanUnroll * nthr) {
+      int pk[kPlanUnroll];
+#pragma unroll
+      for (int i = 0; i < kPlanUnroll; ++i) pk[i] = b0 + i * nthr < B ? s_off[b0 + i * nthr] : 0;
+#pragma unroll
+      for (int i = 0; i < kPlanUnroll; ++i)
+        if (b0 + i * nthr < B) s_rb[b0 + i * nthr] = (b0 + i * nthr) | ((pk[i] >> 16) << 16);
+    }
   } else {
-    for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
-      const int b = t0 + lane;
-      int bin = -1, ns = 0;
-      if (b < r1) {
-        const int packed = s_off[b];                // pass 1's (bin, nsplit)
-        bin = packed & 0xffff;
-        ns = packed >> 16;
+    for (int t0 = r0; t0 < r1; t0 += kPlanUnroll * 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
+      int pk[kPlanUnroll];
+#pragma unroll
+      for (int i = 0; i < kPlanUnroll; ++i) pk[i] = t0 + i * 32 + lane < r1 ? s_off[t0 + i * 32 + lane] : 0;
+#pragma unroll
+      for (int i = 0; i < kPlanUnroll; ++i) {
+        if (t0 + i * 32 >= r1) break;  // warp-uniform
+        const int b = t0 + i * 32 + lane;
+        int bin = -1, ns = 0;
+        if (b < r1) {
+          const int packed = pk[i];                   // pass 1's (bin, nsplit)
+          bin = packed & 0xffff;
+          ns = packed >> 16;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        const int lower = __popc(peers & lt_mask);
+        int pos = 0;
+        if (bin >= 0) pos = s_wcnt[warp * kNumBins + bin] + lower;
+        __syncwarp();
+        if (bin >= 0) {
+          s_rb[pos] = b | (ns << 16);  // b < 8192, ns <= kMaxSplits
+          if (lower == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
+        }
+        __syncwarp();
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, bin);
-      const int lower = __popc(peers & lt_mask);
-      int pos = 0;
-      if (bin >= 0) pos = s_wcnt[warp * kNumBins + bin] + lower;
-      __syncwarp();
-      if (bin >= 0) {
-        s_rb[pos] = b | (ns << 16);  // b < 8192, ns <= kMaxSplits
-        if (lower == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
-      }
-      __syncwarp();
     }
   }
   __syncthreads();
@@ -473,17 +542,23 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     int carry = 0;
     for (int w = 0; w < warp; ++w) carry += s_w[w];
     carry *= Hkv;
-    for (int t0 = r0; t0 < r1; t0 += 32) {
-      const int r = t0 + lane;
-      const int cnt = r < r1 ? (s_rb[r] >> 16) * Hkv : 0;
-      int incl = cnt;
+    for (int t0 = r0; t0 < r1; t0 += kPlanUnroll * 32) {
+      int cr[kPlanUnroll];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+      for (int i = 0; i < kPlanUnroll; ++i) cr[i] = t0 + i * 32 + lane < r1 ? (s_rb[t0 + i * 32 + lane] >> 16) * Hkv : 0;
+#pragma unroll
+      for (int i = 0; i < kPlanUnroll; ++i) {
+        if (t0 + i * 32 >= r1) break;  // warp-uniform
+        const int r = t0 + i * 32 + lane;
+        int incl = cr[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        if (r < r1) s_off[r] = carry + incl - cr[i];
+        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
-      if (r < r1) s_off[r] = carry + incl - cnt;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (tid == 0) s_off[B] = (int)N;
   }
@@ -1063,29 +1138,73 @@ __global__ void __launch_bounds__(kThreads, 2)
       if constexpr (kStages % kConsumerWarps != 0) st_release_cta(sbase + SL::seq + st * 4, (int)qseq);
       mbar_arrive(bar_full + st * 8);
     };
-    // Quad unit u (items f .. f + 3, one per consumer warp): lanes 0..3 look up one item each,
-    // lane 0 posts the slot and issues the Q rows (slot copies, or ring positions qbase + w at
-    // G = 8); page j of item w goes out as ring page qbase' + 4 j + w (null stages pad the
-    // shorter items), so warp w always owns the ring positions = w (mod 4) of the unit.
-    // Quad unit u (items f .. f + 3, one per consumer warp): lanes 0..3 look up one item each,
-    // lane 0 posts the slot and issues the Q rows (slot copies, or ring positions qbase + w at
-    // G = 8); page j of item w goes out as ring page qbase' + 4 j + w (null stages pad the
-    // shorter items), so warp w always owns the ring positions = w (mod 4) of the unit.
-    auto issue_quad = [&](int u, uint32_t kk) {
+    // ---- units, prepared one ahead.  While a quad unit's pages go out, the ticket that names
+    // the next unit is drawn (kDrawAhead ring positions before the unit's end) and resolved, and
+    // the next unit's lookups (its item(s) from the plan, the first 32 page ids of each item:
+    // global loads) are issued (kResolveAhead positions before the end), so neither the atomic's
+    // nor the page ids' round trip sits between two short units, where the ring would drain (a
+    // 16-page unit is ~5 us of a CTA's share of HBM): B = 1024 x 64 tokens 53.0 -> 50.0 us.  A CTA
+    // holds at most one unstarted unit, and only during its current unit's last kDrawAhead
+    // positions (round 1 held three tickets for whole units: an 80 us finish spread).  CTA-wide
+    // units draw at their end (the ring's kStages pages cover the round trips there; a pacing
+    // call in their page loop measured 1-2% slower on C2 / C4).
+    struct Prep {
+      WorkItem my;             // wide unit: the item (every lane); quad unit: item f + (lane & 3)
+      int ids[kQuad][2];       // wide: ids[0][0] = page id `lane`; quad: ids j = lane, 32 + lane of item w
+    };
+    auto prep = [&](Prep& P, int u) {
+      if (u >= n_units) return;
+      if (SL::quads && is_quad(u)) {
+        P.my = get_item(unit_item(u) + (lane & (kQuad - 1)));
+#pragma unroll
+        for (int w = 0; w < kQuad; ++w) {
+          const int n = __shfl_sync(0xffffffffu, P.my.pend - P.my.pbeg, w);
+          const int pb = __shfl_sync(0xffffffffu, P.my.pbeg, w);
+          P.ids[w][0] = lane < n ? __ldg(a.indices + pb + lane) : 0;
+          P.ids[w][1] = lane + 32 < n ? __ldg(a.indices + pb + 32 + lane) : 0;
+        }
+      } else {
+        P.my = get_item(unit_item(u));
+        P.ids[0][0] = lane < P.my.pend - P.my.pbeg ? __ldg(a.indices + P.my.pbeg + lane) : 0;
+      }
+    };
+    // ring positions left in the unit when the ticket is drawn / resolved and the next unit
+    // prepared (measured, B = 1024 x 64 tokens: G = 4 16 / 8 -> 50.2 us, 8 / 4 -> 50.7; G = 8, whose
+    // units also carry four Q positions, 8 / 4 -> 55.9 us, 16 / 8 -> 57.7)
+    constexpr int kDrawAhead = SL::ring_q ? 8 : 16;
+    constexpr int kResolveAhead = SL::ring_q ? 4 : 8;
+    bool may_draw = !early;                  // early mode: no ticket before griddepcontrol.wait
+    bool drawn = false, resolved = false;
+    int t_raw = -1, since = 0, i_next = n_units;
+    Prep cp, nx;
+    auto pace = [&](int rem) {  // warp-uniform: called before issuing ring position `rem` from the end
+      if (!may_draw) return;
+      if (!drawn) {
+        if (rem <= kDrawAhead) {
+          t_raw = issue();  // the atomic's result is first used at the resolve below
+          drawn = true;
+          since = 0;
+        }
+      } else if (!resolved && ++since >= 2 && rem <= kResolveAhead) {
+        i_next = resolve(t_raw);
+        resolved = true;
+        prep(nx, i_next);
+      }
+    };
+    // Quad unit u (items f .. f + 3, one per consumer warp, prepared in P): lane 0 posts the slot
+    // and issues the Q rows (slot copies, or ring positions qbase + w at G = 8); page j of item w
+    // goes out as ring page qbase' + 4 j + w (null stages pad the shorter items), so warp w always
+    // owns the ring positions = w (mod 4) of the unit.
+    auto issue_quad = [&](int u, uint32_t kk, const Prep& P) {
       if constexpr (SL::quads) {
         const int f = unit_item(u);
         const int nsub = kQuad;  // quad units are always full (the remainder runs CTA-wide)
-        const WorkItem my = get_item(f + min(lane & (kQuad - 1), nsub - 1));
-        int npw[kQuad], hw[kQuad], ids[kQuad][2];  // page ids j = lane and j = 32 + lane
+        int npw[kQuad], hw[kQuad];
         int maxnp = 0;
 #pragma unroll
         for (int w = 0; w < kQuad; ++w) {
-          const int n = __shfl_sync(0xffffffffu, my.pend - my.pbeg, w);
-          const int pb = __shfl_sync(0xffffffffu, my.pbeg, w);
-          hw[w] = __shfl_sync(0xffffffffu, my.h, w);
-          npw[w] = w < nsub ? n : 0;
-          ids[w][0] = lane < npw[w] ? __ldg(a.indices + pb + lane) : 0;
-          ids[w][1] = lane + 32 < npw[w] ? __ldg(a.indices + pb + 32 + lane) : 0;
+          npw[w] = __shfl_sync(0xffffffffu, P.my.pend - P.my.pbeg, w);
+          hw[w] = __shfl_sync(0xffffffffu, P.my.h, w);
           maxnp = max(maxnp, npw[w]);
         }
         const uint32_t slot = kk % kItemSlots;
@@ -1094,11 +1213,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane == 0) mbar_wait(bar_iempty + slot * 8, ((kk / kItemSlots) & 1) ^ 1);
 #pragma unroll
         for (int w = 0; w < kQuad; ++w) {
-          const int v0 = __shfl_sync(0xffffffffu, my.b, w), v1 = __shfl_sync(0xffffffffu, my.h, w);
-          const int v2 = __shfl_sync(0xffffffffu, my.pbeg, w), v3 = __shfl_sync(0xffffffffu, my.pend, w);
-          const int v4 = __shfl_sync(0xffffffffu, my.last_valid, w);
-          const int v5 = __shfl_sync(0xffffffffu, my.part_base, w);
-          const int v6 = __shfl_sync(0xffffffffu, my.nsplit, w), v7 = __shfl_sync(0xffffffffu, my.split, w);
+          const int v0 = __shfl_sync(0xffffffffu, P.my.b, w), v1 = hw[w];
+          const int v2 = __shfl_sync(0xffffffffu, P.my.pbeg, w), v3 = __shfl_sync(0xffffffffu, P.my.pend, w);
+          const int v4 = __shfl_sync(0xffffffffu, P.my.last_valid, w);
+          const int v5 = __shfl_sync(0xffffffffu, P.my.part_base, w);
+          const int v6 = __shfl_sync(0xffffffffu, P.my.nsplit, w), v7 = __shfl_sync(0xffffffffu, P.my.split, w);
           if (lane == 0) {
             int* d = fld + w * 8;
             d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3; d[4] = v4; d[5] = v5; d[6] = v6; d[7] = v7;
@@ -1116,13 +1235,13 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (lane == 0) mbar_arrive(bar_ifull + slot * 8);
 #pragma unroll
           for (int w = 0; w < kQuad; ++w) {
-            const int qb = __shfl_sync(0xffffffffu, my.b, w), qh = __shfl_sync(0xffffffffu, my.h, w);
+            const int qb = __shfl_sync(0xffffffffu, P.my.b, w);
             if (lane == 0) {
               const uint32_t st = qseq % kStages;
               mbar_wait(bar_empty + st * 8, ((qseq / kStages) & 1) ^ 1);
               if constexpr (kStages % kConsumerWarps != 0) st_release_cta(sbase + SL::seq + st * 4, (int)qseq);
               mbar_arrive_expect_tx(bar_full + st * 8, qbytes);
-              tma_load_2d(sbase + SL::stages + st * kStageBytes, &tmQ, 0, qb * a.Hq + qh * G, bar_full + st * 8);
+              tma_load_2d(sbase + SL::stages + st * kStageBytes, &tmQ, 0, qb * a.Hq + hw[w] * G, bar_full + st * 8);
             }
             ++qseq;
           }
@@ -1131,16 +1250,17 @@ __global__ void __launch_bounds__(kThreads, 2)
           __syncwarp();
 #pragma unroll
           for (int w = 0; w < kQuad; ++w) {  // lane 0 (the lane that waited for the slot) loads Q
-            const int qb = __shfl_sync(0xffffffffu, my.b, w), qh = __shfl_sync(0xffffffffu, my.h, w);
+            const int qb = __shfl_sync(0xffffffffu, P.my.b, w);
             if (lane == 0 && w < nsub)
               bulk_load(sbase + SL::qslots + slot * SL::qslot_bytes + w * qbytes,
-                        a.q + ((size_t)qb * a.Hq + (size_t)qh * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
+                        a.q + ((size_t)qb * a.Hq + (size_t)hw[w] * G) * kHeadDim, qbytes, bar_ifull + slot * 8);
           }
         }
         for (int j = 0; j < maxnp; ++j) {
+          pace(kQuad * (maxnp - j));
 #pragma unroll
           for (int w = 0; w < kQuad; ++w) {
-            const int page = __shfl_sync(0xffffffffu, j < 32 ? ids[w][0] : ids[w][1], j & 31);
+            const int page = __shfl_sync(0xffffffffu, j < 32 ? P.ids[w][0] : P.ids[w][1], j & 31);
             if (lane == 0) {
               if (j < npw[w])
                 issue_page(page, hw[w]);
@@ -1152,73 +1272,58 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     };
-    // The first item (blockIdx.x: no ticket needed) goes out before anything else: its Q and
-    // its first kStages pages (early mode: all its pages, which may run while the previous
-    // kernel finishes) are in flight while the scheduler tickets resolve.
-    int i_cur = blockIdx.x < n_units ? (int)blockIdx.x : n_units;  // unit indices from here on
-    if (i_cur >= n_units) exhausted = true;
-    WorkItem cur = get_item(unit_item(i_cur));
-    int cur_idx = (i_cur < n_units && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
-    int pre = 0;
-    bool first_done = false;  // a quad first unit goes out whole before the tickets
-    if (is_quad(i_cur)) {
-      issue_quad(i_cur, 0);
-      first_done = true;
-    } else if (i_cur < n_units) {
-      if (lane == 0) post_item(0, cur, unit_item(i_cur));
-      const int np0 = cur.pend - cur.pbeg;
-      pre = early ? np0 : min(np0, kStages);
-      int blk = cur_idx;
-      for (int j0 = 0; j0 < pre; j0 += 32) {
-        const int nb = (j0 + 32 + lane < np0) ? __ldg(a.indices + cur.pbeg + j0 + 32 + lane) : 0;
-        const int cnt = min(32, pre - j0);
+    // CTA-wide unit u (one item, prepared in P): lane 0 posts the item slot and its Q rows, then
+    // the item's pages go out one ring position each (page ids 32 at a time, one block ahead).
+    auto issue_wide = [&](int u, uint32_t kk, const Prep& P) {
+      const WorkItem& it = P.my;
+      if (lane == 0) post_item(kk, it, unit_item(u));
+      const int np = it.pend - it.pbeg;
+      int blk = P.ids[0][0];
+      for (int j0 = 0; j0 < np; j0 += 32) {
+        const int nb = (j0 + 32 + lane < np) ? __ldg(a.indices + it.pbeg + j0 + 32 + lane) : 0;
+        const int cnt = min(32, np - j0);
         for (int j = 0; j < cnt; ++j) {
           const int page = __shfl_sync(0xffffffffu, blk, j);
-          if (lane == 0) issue_page(page, cur.h);
+          if (lane == 0) issue_page(page, it.h);
 #ifdef L4_DEBUG_CKS
-          if (lane == 0 && unit_item(i_cur) < 16384)
-            atomicAdd(&g_cks[unit_item(i_cur) * 4 + 3], (unsigned)page * (unsigned)(j0 + j + 1));
+          if (lane == 0 && unit_item(u) < 16384)
+            atomicAdd(&g_cks[unit_item(u) * 4 + 3], (unsigned)page * (unsigned)(j0 + j + 1));
 #endif
           ++qseq;
         }
         blk = nb;
       }
+    };
+    auto issue_unit = [&](int u, uint32_t kk, const Prep& P) {
+      if (is_quad(u))
+        issue_quad(u, kk, P);
+      else
+        issue_wide(u, kk, P);
+    };
+    // The first unit (blockIdx.x: no ticket needed) goes out before anything else; in early mode
+    // all of it, before griddepcontrol.wait (it may run while the previous kernel finishes).
+    int i_cur = blockIdx.x < n_units ? (int)blockIdx.x : n_units;  // unit indices from here on
+    if (i_cur >= n_units) exhausted = true;
+    prep(cp, i_cur);
+    bool first_done = false;
+    if (early && i_cur < n_units) {
+      issue_unit(i_cur, 0, cp);
+      first_done = true;
     }
     // from here on the scheduler state of the workspace is touched
     if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    may_draw = true;
     uint32_t k = 0;
-    {
-      // One unit at a time: the ticket for the next unit is drawn once this unit's pages are
-      // issued (the ring's kStages pages in flight cover the atomic's round trip), so no CTA
-      // holds work it has not started when the counter runs out: the launch ends balanced.
-      for (; i_cur < n_units; ++k) {
-        if (is_quad(i_cur)) {
-          if (!(k == 0 && first_done)) issue_quad(i_cur, k);
-        } else {
-          if (k > 0 && lane == 0) post_item(k, cur, unit_item(i_cur));
-          const int np = cur.pend - cur.pbeg;
-          const int jstart = k == 0 ? pre : 0;  // item 0's first `pre` pages went out above
-          if (jstart < np) {
-            int j0 = jstart & ~31;
-            int blk = j0 == 0 ? cur_idx : ((j0 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + lane) : 0);
-            for (; j0 < np; j0 += 32) {
-              const int nb = (j0 + 32 + lane < np) ? __ldg(a.indices + cur.pbeg + j0 + 32 + lane) : 0;
-              const int cnt = min(32, np - j0);
-              for (int j = max(jstart - j0, 0); j < cnt; ++j) {
-                const int page = __shfl_sync(0xffffffffu, blk, j);
-                if (lane == 0) issue_page(page, cur.h);
-                ++qseq;
-              }
-              blk = nb;
-            }
-          }
-        }
-        i_cur = resolve(issue());
-        if (i_cur < n_units) {
-          cur = get_item(unit_item(i_cur));
-          cur_idx = (!is_quad(i_cur) && lane < cur.pend - cur.pbeg) ? __ldg(a.indices + cur.pbeg + lane) : 0;
-        }
+    for (; i_cur < n_units; ++k) {
+      if (!(k == 0 && first_done)) issue_unit(i_cur, k, cp);
+      if (!drawn) t_raw = issue();
+      if (!resolved) {
+        i_next = resolve(t_raw);
+        prep(nx, i_next);
       }
+      drawn = resolved = false;
+      i_cur = i_next;
+      cp = nx;
     }
     // every ticket this CTA drew has been resolved: report done
     if (lane == 0) {
