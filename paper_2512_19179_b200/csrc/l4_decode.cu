@@ -109,20 +109,10 @@ static_assert(sizeof(WorkItem) == 32, "WorkItem is 32 bytes");
 // every CTA, built only into trace variants (scripts/build_variant.sh ... -DL4_TRACE).
 __device__ unsigned long long g_trace[4096 * 16];
 __device__ unsigned long long g_trace_last[4096 * 4];  // last CTA-wide item: start, pages, splits, index
-__device__ long long g_trace_clk0[4096];  // clock64 at mark 0 (marks > 0: cycle-exact offsets from it)
-__device__ __forceinline__ void trace_mark(int k) {
-  if (k == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));  // 256 ns granularity on this part
-    g_trace[blockIdx.x * 16] = t;
-    g_trace_clk0[blockIdx.x] = clock64();
-  } else {  // globaltimer of mark 0 + elapsed SM cycles at L4_TRACE_MHZ (the clock under load)
-#ifndef L4_TRACE_MHZ
-#define L4_TRACE_MHZ 1965
-#endif
-    const long long dc = clock64() - *(volatile long long*)&g_trace_clk0[blockIdx.x];
-    g_trace[blockIdx.x * 16 + k] = *(volatile unsigned long long*)&g_trace[blockIdx.x * 16] + dc * 1000 / L4_TRACE_MHZ;
-  }
+__device__ __forceinline__ void trace_mark(int k) {  // globaltimer: 256 ns granularity on this part
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_trace[blockIdx.x * 16 + k] = t;
 }
 #define L4_MARK(k) trace_mark(k)
 __device__ __forceinline__ unsigned long long trace_now() {
@@ -1884,6 +1874,20 @@ extern "C" int l4_trace_read_last(unsigned long long* host, int n) {
 extern "C" int l4_trace_clear(void) {
   static unsigned long long zeros[4096 * 16];
   return (int)cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros));
+}
+__device__ unsigned long long g_trace_stamp[64];
+__global__ void trace_stamp_kernel(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_trace_stamp[slot] = t;
+}
+// stream-ordered globaltimer stamp (a 1-thread kernel): brackets a call on the GPU timeline
+extern "C" int l4_trace_stamp(int slot, void* stream) {
+  trace_stamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(slot);
+  return (int)cudaGetLastError();
+}
+extern "C" int l4_trace_read_stamps(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace_stamp, sizeof(unsigned long long) * (size_t)n);
 }
 #endif
 

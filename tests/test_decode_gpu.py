@@ -175,6 +175,31 @@ def test_plan_covers_every_token_once():
         assert all(a >= b for a, b in zip(bl, bl[1:]))
 
 
+def test_single_bin_fast_path_plan_equals_general_plan():
+    """The planner's fast path (no split request, every request in one length bin: the stable
+    LPT order is the request order) builds the same work list as the general counting-sort path:
+    the same batch plus one shorter request (a second, lower bin, ranked last) takes the general
+    path, and its work list must start with the fast path's, item for item."""
+    rng = np.random.default_rng(21)
+    lens_a = rng.integers(500, 1000, size=300)            # 32..63 pages: one bin (bit_length 6)
+    lens_b = np.concatenate([lens_a, [5]])                 # + one 1-page request (bin 1)
+    plans = []
+    for lens in (lens_a, lens_b):
+        table = synth.make_page_table(lens, seed=0)
+        params = l4.make_params(table.batch, 32, 8)
+        ws = l4.alloc_workspace(params, table.total_pages)
+        l4.decode_plan(params, torch.from_numpy(table.kv_len).cuda(), torch.from_numpy(table.indptr).cuda(),
+                       table.total_pages, ws)
+        plans.append((l4.plan_info(ws), l4.plan_items(ws)))
+    (ia, pa), (ib, pb) = plans
+    assert ia.chunk_pages == ib.chunk_pages and ia.max_splits == ib.max_splits == 1
+    assert len(pa) == 300 * 8 and len(pb) == 301 * 8
+    np.testing.assert_array_equal(pa, pb[: len(pa)])
+    assert pb[-8:, 0].tolist() == [300] * 8                  # the short request comes last
+    assert pa[:, 0].tolist() == np.repeat(np.arange(300), 8).tolist()  # request order, heads ascending
+    assert pa[:, 1].tolist() == np.tile(np.arange(8), 300).tolist()
+
+
 def test_empty_batch_and_all_empty_requests():
     shape, table, q, k, v, ro, rl = _case([0, 0, 0], 8, 2)
     out, lse = _run_gpu(table, q, k, v)
