@@ -225,7 +225,9 @@ def test_bidirectional_precopy_overlaps_next_decode():
                     # keep the device ahead of the host (as in a GPU-bound serving loop): the copy
                     # enqueued by apply() starts when this step's decode ends, while the host has
                     # long enqueued the next step's decode
-                    torch.cuda._sleep(20_000_000)
+                    # (~100 ms of spinning: the host's apply() of step 0 -- thread-hub barriers, pack
+                    # launches -- must finish before this step's decodes end, even on a loaded host)
+                    torch.cuda._sleep(200_000_000)
                     for _ in range(4):
                         l4.decode_attention(q[:B], rt.pool["k"], rt.pool["v"], d_ptr, rt.table, d_len)
                     e1.record()
