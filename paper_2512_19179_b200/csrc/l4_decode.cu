@@ -890,10 +890,17 @@ __device__ __forceinline__ uint32_t slice_off(int t, int cd) {
   return (uint32_t)((cd >> 3) * kHalfBytes + t * 128 + (((cd & 7) ^ (t & 7)) << 4));
 }
 
+#ifndef L4_EARLY_RELEASE
+#define L4_EARLY_RELEASE 1
+#endif
 // One page (16 tokens) of one (request, kv head): S^T = K Q^T, online softmax, O^T += V^T P^T.
+// With L4_EARLY_RELEASE the V fragments are loaded right after the S product and the stage is
+// released to the producer (proxy fence, arrive on `rel_bar`) before the softmax and the PV
+// product, so a stage is held only while it is read and the next TMA into it goes out sooner.
 __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const uint32_t (&qf)[8][2],
                                              float (&acc)[8][4], float (&mrow)[2], float (&lrow)[2],
-                                             float scale_log2, int lane, uint32_t& cks_k, uint32_t& cks_v) {
+                                             float scale_log2, int lane, uint32_t& cks_k, uint32_t& cks_v,
+                                             uint32_t rel_bar) {
   using namespace dev;
   const int g = lane >> 2, c = lane & 3;
   const int mi = lane >> 3, r8 = lane & 7;
@@ -910,6 +917,30 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
       mma_bf16_16816(s, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
     }
   }
+#if L4_EARLY_RELEASE
+  uint32_t vf[8][4];
+  {
+    const int tok = r8 + ((mi >> 1) << 3);
+    const uint32_t vbase = sbase + kSliceBytes;
+    // masks for invalid tokens of a partial last page (V may hold NaN there)
+    const uint32_t mlo = (((2 * c) < valid) ? 0x0000ffffu : 0u) | (((2 * c + 1) < valid) ? 0xffff0000u : 0u);
+    const uint32_t mhi = (((2 * c + 8) < valid) ? 0x0000ffffu : 0u) | (((2 * c + 9) < valid) ? 0xffff0000u : 0u);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      ldmatrix_x4_trans(vbase + slice_off(tok, mt * 2 + (mi & 1)), vf[mt][0], vf[mt][1], vf[mt][2], vf[mt][3]);
+      if (valid < kPage) {
+        vf[mt][0] &= mlo;
+        vf[mt][1] &= mlo;
+        vf[mt][2] &= mhi;
+        vf[mt][3] &= mhi;
+      }
+      cks_v ^= vf[mt][0] ^ vf[mt][1] ^ vf[mt][2] ^ vf[mt][3];
+    }
+  }
+  fence_proxy_async_smem();  // this warp's reads of the stage before the producer's next TMA into it
+  __syncwarp();
+  if (lane == 0) mbar_arrive(rel_bar);
+#endif
   // ---- mask (Z20: tokens >= kv_len are not attended) and online softmax in the exp2 domain
   const float NEG = -INFINITY;
   const float t0 = (g < valid) ? s[0] * scale_log2 : NEG;
@@ -944,6 +975,13 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
   const uint32_t bh0 = movmatrix_trans(h0), bh1 = movmatrix_trans(h1);
   const uint32_t bl0 = movmatrix_trans(l0), bl1 = movmatrix_trans(l1);
   // ---- O^T[128 d x 8 heads] += V^T[128 x 16 tok] * P^T[16 tok x 8 heads]
+#if L4_EARLY_RELEASE
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    mma_bf16_16816(acc[mt], vf[mt][0], vf[mt][1], vf[mt][2], vf[mt][3], bh0, bh1);
+    mma_bf16_16816(acc[mt], vf[mt][0], vf[mt][1], vf[mt][2], vf[mt][3], bl0, bl1);
+  }
+#else
   {
     const int tok = r8 + ((mi >> 1) << 3);
     const uint32_t vbase = sbase + kSliceBytes;
@@ -965,6 +1003,10 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
       mma_bf16_16816(acc[mt], a0, a1, a2, a3, bl0, bl1);
     }
   }
+  fence_proxy_async_smem();  // this warp's reads of the stage before the producer's next TMA into it
+  __syncwarp();
+  if (lane == 0) mbar_arrive(rel_bar);
+#endif
 }
 
 __device__ __forceinline__ WorkItem load_item(const WorkItem* items, int i, int n) {
@@ -1458,12 +1500,13 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         mbar_wait(bar_full + st * 8, (q / kStages) & 1);
-        if (j < np)
+        if (j < np) {  // consume_page releases the stage
           consume_page(sbase + SL::stages + st * kStageBytes, (j == np - 1) ? it.last_valid : kPage, qf, acc, mrow,
-                       lrow, a.scale_log2, lane, cks_k, cks_v);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_empty + st * 8);
+                       lrow, a.scale_log2, lane, cks_k, cks_v, bar_empty + st * 8);
+        } else {  // a null stage (nothing was read)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_empty + st * 8);
+        }
       }
       qbase += kQuad * maxnp;
       if (early && k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
@@ -1566,13 +1609,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef L4_TRACE
       const unsigned long long tc0 = trace_now();
 #endif
-      consume_page(sbase + SL::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane, cks_k, cks_v);
+      consume_page(sbase + SL::stages + st * kStageBytes, valid, qf, acc, mrow, lrow, a.scale_log2, lane, cks_k, cks_v,
+                   bar_empty + st * 8);  // releases the stage
 #ifdef L4_TRACE
       if (warp == 0 && lane == 0) trace_add(11, trace_now() - tc0);
 #endif
-      fence_proxy_async_smem();  // this warp's reads of the stage before the producer's next TMA into it
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_empty + st * 8);
     }
     qbase += np;
     if (early && k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
