@@ -73,6 +73,10 @@ constexpr int kMinChunk = 8;                          // pages
 #define L4_ITEMS_PER_CTA 8
 #endif
 constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
+#ifndef L4_ITEMS_PER_CTA_ALL_SPLIT
+#define L4_ITEMS_PER_CTA_ALL_SPLIT 12
+#endif
+constexpr int kItemsPerCtaAllSplit = L4_ITEMS_PER_CTA_ALL_SPLIT;  // ... when every request is split
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
@@ -225,9 +229,9 @@ int items_cap_for(const l4_decode_params* p, int64_t max_total_pages, int num_ct
   } else if (p->chunk_pages > 0) {
     cap = Hkv * (B + ceil_div64(max_total_pages, p->chunk_pages));
   } else {
-    // C >= T*Hkv/(W*k) => Hkv * sum ceil(p_b / C) <= W*k + Hkv*B
+    // C >= T*Hkv/(W*k) => Hkv * sum ceil(p_b / C) <= W*k + Hkv*B (k: the larger chunk target)
     cap = std::min(Hkv * (B + ceil_div64(max_total_pages, kMinChunk)),
-                   Hkv * B + (int64_t)num_ctas * kItemsPerCta + Hkv);
+                   Hkv * B + (int64_t)num_ctas * std::max(kItemsPerCta, kItemsPerCtaAllSplit) + Hkv);
   }
   cap = std::max<int64_t>(cap, 1);
   return (int)std::min<int64_t>(cap, INT_MAX / 64);
@@ -246,34 +250,38 @@ struct PlanArgs {
 constexpr int kPlanMaxWarps = kPlanThreads / 32;
 constexpr int kPlanUnroll = 8;  // request tiles per warp whose shared loads the planner issues together
 
-// Block-wide (sum int64, max int, or bits) in one pass.
-__device__ void block_reduce3(long long v, int m, unsigned bits, long long* s_ll, int* s_i, unsigned* s_u,
-                              long long* sum_out, int* max_out, unsigned* or_out) {
+// Block-wide (sum int64, max int, min int, or bits) in one pass.
+__device__ void block_reduce4(long long v, int m, int mn, unsigned bits, long long* s_ll, int* s_i, int* s_mn,
+                              unsigned* s_u, long long* sum_out, int* max_out, int* min_out, unsigned* or_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     v += __shfl_xor_sync(0xffffffffu, v, o);
     m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     bits |= __shfl_xor_sync(0xffffffffu, bits, o);
   }
   __syncthreads();
   if (lane == 0) {
     s_ll[warp] = v;
     s_i[warp] = m;
+    s_mn[warp] = mn;
     s_u[warp] = bits;
   }
   __syncthreads();
   long long t = 0;
-  int mm = 0;
+  int mm = 0, mi = INT_MAX;
   unsigned bb = 0;
 #pragma unroll 8
   for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
     t += s_ll[i];
     mm = max(mm, s_i[i]);
+    mi = min(mi, s_mn[i]);
     bb |= s_u[i];
   }
   *sum_out = t;
   *max_out = mm;
+  *min_out = mi;
   *or_out = bb;
 }
 
@@ -291,7 +299,7 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
 }
 
 // Shared-memory scratch of plan_core (bytes; 8-byte aligned base).
-constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4 + 32 * 4;
+constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4 + 32 * 4 + 32 * 4;
 
 // The planner (a1), run by every thread of a CTA: reads kv_len / indptr, chooses the chunk C,
 // and orders the requests by length bin, longest bin first, request index ascending inside a
@@ -312,15 +320,16 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   int* s_w = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4);        // per-warp sums
   int* s_wcnt = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4);  // [nw][kNumBins]
   int* s_ms = s_wcnt + kPlanMaxWarps * kNumBins;  // per-warp lowest bin of a split request
+  int* s_mn = s_ms + 32;                           // per-warp smallest page count
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nw = nthr >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   long long T;
-  int Pmax;
+  int Pmax, Pmin;
   unsigned bins_seen;  // bit k: some request's unsplit bin (bit_length of its pages) is k
   {
     long long sum = 0;
-    int mx = 0;
+    int mx = 0, mn = INT_MAX;
     unsigned seen = 0u;
     auto take = [&](int b, int Lv, int Pv) {
       s_len[b] = Lv;
@@ -328,6 +337,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
       const int pg = pages_of(Lv);
       sum += pg;
       mx = max(mx, pg);
+      mn = min(mn, pg);
       seen |= 1u << bin_of(pg, 1);
     };
     // one round of loads: 16-byte vectors of both arrays (B <= 1024 needs <= 2 per thread at
@@ -368,7 +378,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
       }
     }
     for (int x = tid; x < nw * kNumBins; x += nthr) s_wcnt[x] = 0;
-    block_reduce3(sum, mx, seen, s_ll, s_i, s_u, &T, &Pmax, &bins_seen);  // its barriers publish s_len/s_ptr
+    block_reduce4(sum, mx, mn, seen, s_ll, s_i, s_mn, s_u, &T, &Pmax, &Pmin, &bins_seen);  // its barriers publish s_len/s_ptr
   }
   if (tid == 0) L4_MARK(6);
   // chunk size C (pages per work item)
@@ -378,11 +388,19 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   } else if (forced_chunk < 0) {
     Cl = INT_MAX / 4;
   } else {
-    const long long denom = (long long)num_ctas * kItemsPerCta;
-    const long long num = T * Hkv + denom - 1;
     // 32-bit division when it fits (a 64-bit one is a long software sequence on the critical path)
-    const long long q = num < (1ll << 31) ? (long long)((unsigned)num / (unsigned)denom) : num / denom;
-    Cl = max((long long)kMinChunk, q);
+    auto chunk_for = [&](int items_per_cta) -> long long {
+      const long long denom = (long long)num_ctas * items_per_cta;
+      const long long num = T * Hkv + denom - 1;
+      const long long q = num < (1ll << 31) ? (long long)((unsigned)num / (unsigned)denom) : num / denom;
+      return max((long long)kMinChunk, q);
+    };
+    Cl = chunk_for(kItemsPerCta);
+    // A batch whose every request is split (a long-context batch: C4, an L4 long-range stage)
+    // has no short unsplit items to fill the end of the launch: finer chunks shorten its tail
+    // (measured, plain calls, items per CTA 8 -> 12: C4 1596 -> 1588 us, 25 x 39454 tokens
+    // 596 -> 590, 12 x 84547 614 -> 605; mixed batches such as C3 keep 8: 12 cost them 0.6%)
+    if (B > 0 && (long long)Pmin > kNoSplitFactor * Cl) Cl = chunk_for(kItemsPerCtaAllSplit);
   }
   Cl = max(Cl, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
   int C = (int)min(Cl, (long long)(INT_MAX / 4));
@@ -449,7 +467,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
       wms = min(wms, __shfl_xor_sync(0xffffffffu, wms, o));
     }
     if (lane == 0) {
-      s_w[warp] = wsum;  // not s_i: slower warps may still read block_reduce3's s_i
+      s_w[warp] = wsum;  // not s_i: slower warps may still read block_reduce4's s_i
       s_ms[warp] = wms;
     }
     __syncthreads();
