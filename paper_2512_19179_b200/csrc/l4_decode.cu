@@ -920,6 +920,11 @@ __device__ __forceinline__ void consume_page(uint32_t sbase, int valid, const ui
                                              float scale_log2, int lane, uint32_t& cks_k, uint32_t& cks_v,
                                              uint32_t rel_bar) {
   using namespace dev;
+#ifdef L4_NO_COMPUTE  // measurement-only: the data-movement skeleton (ring, scheduling) without the math
+  __syncwarp();
+  if (lane == 0) mbar_arrive(rel_bar);
+  return;
+#endif
   const int g = lane >> 2, c = lane & 3;
   const int mi = lane >> 3, r8 = lane & 7;
 
