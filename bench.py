@@ -276,6 +276,34 @@ def steady_ms(wl: Workload, steps: int, warmup: int, early: bool = False, early_
     return e0.elapsed_time(e1) / steps
 
 
+def per_layer_ms(wl: Workload, steps: int, warmup: int, layers: int):
+    """A decode step of a `layers`-layer model: one l4_decode_plan (the work list depends only on
+    the page table, shared by every layer) and `layers` l4_decode_run calls over rotating input
+    copies (each layer reads its own K/V); device time per layer (one event pair around `steps`
+    steps)."""
+    import torch
+    l4, params, ws = make_l4(wl)
+
+    def step():
+        q, k, v, ip, ix, kl = wl.sets[0]
+        l4.decode_plan(params, kl, ip, wl.table.total_pages, ws)
+        for j in range(layers):
+            q, k, v, ip, ix, kl = wl.sets[j % len(wl.sets)]
+            l4.decode_run(params, q, k, v, ix, wl.out, wl.lse, ws)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (steps * layers)
+
+
 _FLUSH = {}
 
 
@@ -645,6 +673,8 @@ def single_gpu_line(args, rank, world, local):
     early = steady_ms(wl, args.steps, args.warmup, early=True)
     eplan = steady_ms(wl, args.steps, args.warmup, early_plan=True)
     cold = cold_ms(wl)
+    n_layers = 80 if wl.shape.num_q_heads == 64 else 32
+    per_layer = per_layer_ms(wl, max(2, args.steps // 4), 1, n_layers) if len(wl.lens) <= 1024 else None
     info = plan_of(wl)
     e2e_steps = max(50, args.steps)
     e2e_ms, h2d, d2h, host_us, e2e_ok = time_e2e(wl, e2e_steps)
@@ -673,6 +703,13 @@ def single_gpu_line(args, rank, world, local):
             args.workload + "_early_plan": {"ms": round(eplan, 5),
                                             "frac": round(wl.bytes_algo / (eplan / 1e3) / 1e9 / peak, 4)},
             **roof}
+    if per_layer:
+        roof[args.workload + f"_per_layer_{n_layers}"] = {
+            "ms": round(per_layer, 5), "kv_gbs": round(wl.bytes_kv / (per_layer / 1e3) / 1e9, 1),
+            "frac": round(wl.bytes_algo / (per_layer / 1e3) / 1e9 / peak, 4),
+            "how": f"one decode step of a {n_layers}-layer model: 1 l4_decode_plan + {n_layers} l4_decode_run "
+                   "(the work list is shared by every layer; each layer reads its own K/V, rotating copies); "
+                   "device time per layer"}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
