@@ -537,6 +537,10 @@ def extra_lines(steps: int, warmup: int, peak: float):
         e = roofline_entry(wl, ms, peak, traffic_key)
         e["cold_ms"] = round(cold, 5)
         e["cold_frac"] = round(wl.bytes_algo / (cold / 1e3) / 1e9 / peak, 4)
+        layers = 80 if wl.shape.num_q_heads == 64 else 32
+        pl = per_layer_ms(wl, 2, 1, layers)  # 1 plan + `layers` runs per step (see per_layer_ms)
+        e[f"per_layer_{layers}_ms"] = round(pl, 5)
+        e[f"per_layer_{layers}_kv_gbs"] = round(wl.bytes_kv / (pl / 1e3) / 1e9, 1)
         roof[name] = e
         return e
 

@@ -83,8 +83,8 @@ constexpr int kPlanThreads = 1024;
 constexpr int kNumBins = 32;
 // Warp-item ("quad") units: unsplit items of at most 2^kQuadBin - 1 pages are scheduled four at
 // a time, one whole item per consumer warp (no cross-warp merge, no CTA barrier per item).
-// 0 disables them.  G <= 4: the four items' Q rows sit in the unit slot; G = 8: they travel
-// through the page ring (a 2-D TMA box each, four ring positions ahead of the pages).
+// 0 disables them.  G <= 4: the four items' Q rows sit in the unit slot; G = 8: each consumer
+// warp loads its item's Q rows from global memory into its mma fragments.
 #ifndef L4_QUAD_BIN
 #define L4_QUAD_BIN 6
 #endif
@@ -744,11 +744,11 @@ template <int G>
 struct SmemLayout {
   static constexpr int stages_n = G == 8 ? 8 : L4_STAGES_SMALL_G;
   static constexpr bool quads = kQuadBin > 0;
-  // G <= 4: a unit slot holds the Q rows of four items (+12 KB at G = 4); G = 8: the four Q
-  // row blocks travel through the page ring instead (four ring positions ahead of the pages)
-  static constexpr bool ring_q = G > kQuadMaxG;
-  static constexpr int qslot_bytes = (quads && !ring_q ? kQuad : 1) * G * kHeadDim * 2;  // Q rows of one unit
-  static_assert(!ring_q || G * kHeadDim * 2 <= kStageBytes, "Q rows fit one ring stage");
+  // G <= 4: a unit slot holds the Q rows of four items (+12 KB at G = 4); G = 8: four items' Q
+  // rows would not fit 2 CTAs/SM (+24 KB), so each consumer warp loads its quad item's rows from
+  // global memory straight into its mma fragments
+  static constexpr bool q_global = G > kQuadMaxG;
+  static constexpr int qslot_bytes = (quads && !q_global ? kQuad : 1) * G * kHeadDim * 2;  // Q rows of one unit
   static constexpr int merge_bytes =
       align16c(cmax(kConsumerWarps * G * kMergeStride * 4, cmax(kPlanScratchBytes, kCombineScratchBytes)));
   static constexpr int stages = 0;
@@ -1048,8 +1048,7 @@ __device__ __forceinline__ WorkItem load_item(const WorkItem* items, int i, int 
 
 template <int G, bool kFused>
 __global__ void __launch_bounds__(kThreads, 2)
-    decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                  const __grid_constant__ CUtensorMap tmQ, RunArgs a) {
+    decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, RunArgs a) {
   using namespace dev;
   using SL = SmemLayout<G>;
   constexpr int kStages = SL::stages_n;
@@ -1085,7 +1084,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kConsumerWarps && lane == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
-    if constexpr (SmemLayout<G>::quads && SmemLayout<G>::ring_q) prefetch_tmap(&tmQ);
   }
   __syncthreads();
   // PDL: the next kernel in the stream may start its prologue as CTAs of this one retire; it
@@ -1244,10 +1242,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     };
     // ring positions left in the unit when the ticket is drawn / resolved and the next unit
-    // prepared (measured, B = 1024 x 64 tokens: G = 4 16 / 8 -> 50.2 us, 8 / 4 -> 50.7; G = 8, whose
-    // units also carry four Q positions, 8 / 4 -> 55.9 us, 16 / 8 -> 57.7)
-    constexpr int kDrawAhead = SL::ring_q ? 8 : 16;
-    constexpr int kResolveAhead = SL::ring_q ? 4 : 8;
+    // prepared (measured, B = 1024 x 64 tokens: G = 4 16 / 8 -> 50.2 us, 8 / 4 -> 50.7; G = 8
+    // 16 / 8 -> 48.2 us, 8 / 4 -> 48.5)
+    constexpr int kDrawAhead = 16;
+    constexpr int kResolveAhead = 8;
     bool may_draw = !early;                  // early mode: no ticket before griddepcontrol.wait
     bool drawn = false, resolved = false;
     int t_raw = -1, since = 0, i_next = n_units;
@@ -1267,7 +1265,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     };
     // Quad unit u (items f .. f + 3, one per consumer warp, prepared in P): lane 0 posts the slot
-    // and issues the Q rows (slot copies, or ring positions qbase + w at G = 8); page j of item w
+    // and issues the Q rows into it (G <= 4; at G = 8 the consumers load them); page j of item w
     // goes out as ring page qbase' + 4 j + w (null stages pad the shorter items), so warp w always
     // owns the ring positions = w (mod 4) of the unit.
     auto issue_quad = [&](int u, uint32_t kk, const Prep& P) {
@@ -1305,21 +1303,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncwarp();
         const uint32_t qbytes = G * kHeadDim * 2;
-        if constexpr (SL::ring_q) {
-          // slot published without data; item w's Q rows go to ring position qbase + w
+        if constexpr (SL::q_global) {
+          // slot published without data: the consumer warps load their items' Q rows themselves
           if (lane == 0) mbar_arrive(bar_ifull + slot * 8);
-#pragma unroll
-          for (int w = 0; w < kQuad; ++w) {
-            const int qb = __shfl_sync(0xffffffffu, P.my.b, w);
-            if (lane == 0) {
-              const uint32_t st = qseq % kStages;
-              mbar_wait(bar_empty + st * 8, ((qseq / kStages) & 1) ^ 1);
-              if constexpr (kStages % kConsumerWarps != 0) st_release_cta(sbase + SL::seq + st * 4, (int)qseq);
-              mbar_arrive_expect_tx(bar_full + st * 8, qbytes);
-              tma_load_2d(sbase + SL::stages + st * kStageBytes, &tmQ, 0, qb * a.Hq + hw[w] * G, bar_full + st * 8);
-            }
-            ++qseq;
-          }
         } else {
           if (lane == 0) mbar_arrive_expect_tx(bar_ifull + slot * 8, nsub * qbytes);
           __syncwarp();
@@ -1490,19 +1476,17 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
       };
-      if constexpr (SL::ring_q) {
-        mbar_arrive(bar_iempty + slot * 8);
-        const uint32_t q = qbase + warp, st = q % kStages;  // this warp's Q rows: ring position qbase + warp
-        if constexpr (kStages % kConsumerWarps != 0) {
-          while (ld_acquire_cta(sbase + SL::seq + st * 4) != (int)q) {
-          }
+      if constexpr (SL::q_global) {
+        // G = 8: the item's 8 Q rows straight from global memory into the mma B fragments (16
+        // independent 4-byte loads per lane, in flight while the item's first page arrives), so
+        // no ring position carries 2 KB of Q in an 8 KB stage
+        mbar_arrive(bar_iempty + slot * 8);  // the slot was read above
+        const __nv_bfloat16* qr = a.q + ((size_t)it.b * a.Hq + (size_t)it.h * G + g) * kHeadDim;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          qf[kk][0] = __ldg(reinterpret_cast<const unsigned*>(qr + kk * 16 + 2 * c));
+          qf[kk][1] = __ldg(reinterpret_cast<const unsigned*>(qr + kk * 16 + 8 + 2 * c));
         }
-        mbar_wait(bar_full + st * 8, (q / kStages) & 1);
-        load_qf(smem + SL::stages + st * kStageBytes);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_empty + st * 8);
-        qbase += kQuad;
       } else {
         load_qf(smem + SL::qslots + slot * SL::qslot_bytes + warp * (G * kHeadDim * 2));
         fence_proxy_async_smem();  // Q-slot reads before the producer's next bulk copy into the slot
@@ -1790,23 +1774,6 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-// q [B, Hq, 128] bf16 as rows of 128 elements; box = G rows (no swizzle: lands as the G x 256 B
-// block the consumers read with plain shared loads).  Used by the G = 8 quad units (ring_q).
-l4_status make_qmap(CUtensorMap* tm, const void* q, int64_t rows, int G) {
-  auto enc = get_encode_fn();
-  if (!enc) return fail(L4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no device)");
-  if (rows <= 0 || rows > ((int64_t)1 << 31)) return fail(L4_ERR_INVALID_ARG, "q too large for a tensor map");
-  cuuint64_t dims[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kHeadDim * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kHeadDim, (cuuint32_t)G};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(q), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(L4_ERR_INVALID_ARG, "cuTensorMapEncodeTiled(q) failed");
-  return L4_OK;
-}
-
 // Pool [num_pages, Hkv, 16, 128] bf16 viewed as a 3-D tensor
 // (64 columns, num_pages*Hkv*16 rows of 256 B, 2 column halves 128 B apart);
 // one box = 64 x 16 x 2 = one whole (page, kv head) slice of 4 KB, landing in
@@ -1831,7 +1798,7 @@ l4_status make_tmap(CUtensorMap* tm, const void* base, int64_t rows) {
 }
 
 template <int G, bool kFused>
-l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tq, const RunArgs& a,
+l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const RunArgs& a,
                         int grid, cudaStream_t st) {
   static std::atomic<bool> attr_set[64];  // per device; cudaFuncSetAttribute is idempotent
   const size_t smem_max = SmemLayout<G>::alloc + (kFused ? fused_plan_bytes(kFusedMaxBatch) : 0);
@@ -1860,7 +1827,7 @@ l4_status launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const CUte
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<G, kFused>, tk, tv, tq, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<G, kFused>, tk, tv, a);
   if (e != cudaSuccess) {
     set_error("decode_kernel launch failed: %s", cudaGetErrorString(e));
     cudaGetLastError();
@@ -2078,13 +2045,6 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   if (s != L4_OK) return s;
   s = make_tmap(&tv, v_pages, rows);
   if (s != L4_OK) return s;
-  // q [B * Hq rows of 256 B]: one box = the G query rows of a kv group (2-D TMA); read only by
-  // the G = 8 quad units (ring_q), so the other group sizes skip the host-side encode
-  CUtensorMap tq = tk;
-  if (G > kQuadMaxG && kQuadBin > 0) {
-    s = make_qmap(&tq, q, (int64_t)p->batch * p->num_q_heads, G);
-    if (s != L4_OK) return s;
-  }
   char* ws = static_cast<char*>(workspace);
   RunArgs a;
   memset(&a, 0, sizeof(a));
@@ -2112,17 +2072,17 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   a.early = !fused ? 0 : (p->flags & L4_DECODE_EARLY_INPUTS) ? 1 : (p->flags & L4_DECODE_EARLY_PLAN) ? 2 : 0;
   if (fused) {
     switch (G) {
-      case 1: return launch_decode<1, true>(tk, tv, tq, a, ctas, st);
-      case 2: return launch_decode<2, true>(tk, tv, tq, a, ctas, st);
-      case 4: return launch_decode<4, true>(tk, tv, tq, a, ctas, st);
-      default: return launch_decode<8, true>(tk, tv, tq, a, ctas, st);
+      case 1: return launch_decode<1, true>(tk, tv, a, ctas, st);
+      case 2: return launch_decode<2, true>(tk, tv, a, ctas, st);
+      case 4: return launch_decode<4, true>(tk, tv, a, ctas, st);
+      default: return launch_decode<8, true>(tk, tv, a, ctas, st);
     }
   }
   switch (G) {
-    case 1: return launch_decode<1, false>(tk, tv, tq, a, ctas, st);
-    case 2: return launch_decode<2, false>(tk, tv, tq, a, ctas, st);
-    case 4: return launch_decode<4, false>(tk, tv, tq, a, ctas, st);
-    default: return launch_decode<8, false>(tk, tv, tq, a, ctas, st);
+    case 1: return launch_decode<1, false>(tk, tv, a, ctas, st);
+    case 2: return launch_decode<2, false>(tk, tv, a, ctas, st);
+    case 4: return launch_decode<4, false>(tk, tv, a, ctas, st);
+    default: return launch_decode<8, false>(tk, tv, a, ctas, st);
   }
 }
 
