@@ -88,6 +88,9 @@ constexpr int kNumBins = 32;
 #ifndef L4_QUAD_BIN
 #define L4_QUAD_BIN 6
 #endif
+#ifndef L4_PREFETCH_INPUTS
+#define L4_PREFETCH_INPUTS 1
+#endif
 constexpr int kQuadBin = L4_QUAD_BIN;
 static_assert(kQuadBin >= 0 && kQuadBin <= 6, "quad items hold at most 63 page ids (two per lane)");
 constexpr int kQuadMaxG = 4;
@@ -714,6 +717,7 @@ struct RunArgs {
   int B, forced_chunk, items_cap;
   int quad_bin;  // kQuadBin (0: no quad units)
   int early;  // 1: L4_DECODE_EARLY_INPUTS, 2: L4_DECODE_EARLY_PLAN (fused path), 0: neither
+  long long n_indices;  // page_indices entries (fused path; 0: unknown, no prefetch)
 };
 
 struct __align__(16) SlotItem {  // unit handed from the producer to the consumers
@@ -1084,6 +1088,29 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kConsumerWarps && lane == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
+#if L4_PREFETCH_INPUTS
+    // L2 prefetch of the inputs the prologue reads first — this CTA's share of the page ids and
+    // of q, and (CTA 0) kv_len / indptr — so the plan's loads, the first units' page-id loads and
+    // Q copies hit L2.  A hint, safe before griddepcontrol.wait even in plain mode: L2 is the
+    // point of coherence, so a write of the previous kernel supersedes a prefetched line.
+    const int W0 = gridDim.x;
+    auto pf_share = [&](const void* base, long long bytes) {
+      if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || bytes < 16) return;
+      const long long share = ((bytes + W0 - 1) / W0 + 15) & ~15ll;
+      const long long off = share * blockIdx.x;
+      const long long len = min(share, bytes - off) & ~15ll;
+      if (len > 0) prefetch_l2_bulk(static_cast<const char*>(base) + off, (uint32_t)len);
+    };
+    pf_share(a.indices, a.n_indices * 4);
+    pf_share(a.q, (long long)a.B * a.Hq * kHeadDim * 2);
+    if (kFused && blockIdx.x == 0) {
+      const long long b16 = ((long long)a.B * 4) & ~15ll;
+      if (b16 > 0 && ((reinterpret_cast<uintptr_t>(a.kv_len) | reinterpret_cast<uintptr_t>(a.indptr)) & 15) == 0) {
+        prefetch_l2_bulk(a.kv_len, (uint32_t)b16);
+        prefetch_l2_bulk(a.indptr, (uint32_t)b16);
+      }
+    }
+#endif
   }
   __syncthreads();
   // PDL: the next kernel in the stream may start its prologue as CTAs of this one retire; it
@@ -2070,6 +2097,7 @@ static l4_status run_impl(const l4_decode_params* p, const void* q, const void* 
   a.items_cap = L.items_cap;
   a.quad_bin = kQuadBin;
   a.early = !fused ? 0 : (p->flags & L4_DECODE_EARLY_INPUTS) ? 1 : (p->flags & L4_DECODE_EARLY_PLAN) ? 2 : 0;
+  a.n_indices = fused ? total_pages : 0;
   if (fused) {
     switch (G) {
       case 1: return launch_decode<1, true>(tk, tv, a, ctas, st);
