@@ -77,6 +77,7 @@ constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
 #define L4_ITEMS_PER_CTA_ALL_SPLIT 12
 #endif
 constexpr int kItemsPerCtaAllSplit = L4_ITEMS_PER_CTA_ALL_SPLIT;  // ... when every request is split
+constexpr int kAllSplitMinChunk = 128;  // ... and the default chunk has at least this many pages
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
@@ -399,11 +400,14 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
       return max((long long)kMinChunk, q);
     };
     Cl = chunk_for(kItemsPerCta);
-    // A batch whose every request is split (a long-context batch: C4, an L4 long-range stage)
-    // has no short unsplit items to fill the end of the launch: finer chunks shorten its tail
-    // (measured, plain calls, items per CTA 8 -> 12: C4 1596 -> 1588 us, 25 x 39454 tokens
-    // 596 -> 590, 12 x 84547 614 -> 605; mixed batches such as C3 keep 8: 12 cost them 0.6%)
-    if (B > 0 && (long long)Pmin > kNoSplitFactor * Cl) Cl = chunk_for(kItemsPerCtaAllSplit);
+    // A large batch whose every request is split (a long-context batch: C4, an L4 long-range
+    // stage) has no short unsplit items to fill the end of the launch: finer chunks shorten its
+    // tail (measured, plain calls, items per CTA 8 -> 12: C4 1596 -> 1588 us, 25 x 39454 tokens
+    // 596 -> 590, 12 x 84547 614 -> 605; mixed batches such as C3 keep 8: 12 cost them 0.6%).
+    // Small all-split batches (chunk < kAllSplitMinChunk pages: 22 x ~5K or 3 x ~30K tokens)
+    // are combine- and latency-bound and lost 10-15% with the finer chunk: they keep 8.
+    if (B > 0 && Cl >= kAllSplitMinChunk && (long long)Pmin > kNoSplitFactor * Cl)
+      Cl = chunk_for(kItemsPerCtaAllSplit);
   }
   Cl = max(Cl, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
   int C = (int)min(Cl, (long long)(INT_MAX / 4));
