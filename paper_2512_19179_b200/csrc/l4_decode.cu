@@ -78,6 +78,7 @@ constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
 #endif
 constexpr int kItemsPerCtaAllSplit = L4_ITEMS_PER_CTA_ALL_SPLIT;  // ... when every request is split
 constexpr int kAllSplitMinChunk = 128;  // ... and the default chunk has at least this many pages
+constexpr int kChunkCands = 16;         // chunk candidates of a large all-split batch
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
@@ -303,7 +304,8 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
 }
 
 // Shared-memory scratch of plan_core (bytes; 8-byte aligned base).
-constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4 + 32 * 4 + 32 * 4;
+constexpr int kPlanScratchBytes =
+    32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * 16 * 8;
 
 // The planner (a1), run by every thread of a CTA: reads kv_len / indptr, chooses the chunk C,
 // and orders the requests by length bin, longest bin first, request index ascending inside a
@@ -325,6 +327,7 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   int* s_wcnt = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4);  // [nw][kNumBins]
   int* s_ms = s_wcnt + kPlanMaxWarps * kNumBins;  // per-warp lowest bin of a split request
   int* s_mn = s_ms + 32;                           // per-warp smallest page count
+  long long* s_cand = reinterpret_cast<long long*>(s_mn + 32);  // [nw][kChunkCands] item counts
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nw = nthr >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -401,13 +404,57 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     };
     Cl = chunk_for(kItemsPerCta);
     // A large batch whose every request is split (a long-context batch: C4, an L4 long-range
-    // stage) has no short unsplit items to fill the end of the launch: finer chunks shorten its
-    // tail (measured, plain calls, items per CTA 8 -> 12: C4 1596 -> 1588 us, 25 x 39454 tokens
-    // 596 -> 590, 12 x 84547 614 -> 605; mixed batches such as C3 keep 8: 12 cost them 0.6%).
-    // Small all-split batches (chunk < kAllSplitMinChunk pages: 22 x ~5K or 3 x ~30K tokens)
-    // are combine- and latency-bound and lost 10-15% with the finer chunk: they keep 8.
-    if (B > 0 && Cl >= kAllSplitMinChunk && (long long)Pmin > kNoSplitFactor * Cl)
-      Cl = chunk_for(kItemsPerCtaAllSplit);
+    // stage) has no short unsplit items to fill the end of the launch, so how full its last round
+    // of items is decides its tail: with N items over W CTAs, a last round that only a few CTAs
+    // enter (N / W just above an integer) leaves the rest idle for a whole item, and one that
+    // most CTAs enter evens out their progress spread.  Measured (plain calls, forced chunks):
+    // C4 1544-1563 us when frac(N / W) is 0.73-0.97, 1566-1570 at 0.3-0.4, 1578-1601 at
+    // 0.03-0.22; 25 x 39454 tokens 570 us at 0.78-0.81 vs 584-587 at 0.11-0.16; 12 x 84547 587
+    // at 0.84 vs 606-608 at 0.08-0.11.  So among chunks from the 12-items-per-CTA chunk up to
+    // 1.3x the default one the planner takes the chunk whose last round is closest to 85% full
+    // (ties: the larger chunk, fewer combines).  A/B against a fixed 12 items per CTA (same box):
+    // C4 1588 -> 1571 us, 25 x 39454 591 -> 586, 64 x 16384 623 -> 619, 12 x 84547 and 8 x 131072
+    // unchanged.  Small all-split batches (default chunk < kAllSplitMinChunk pages) are combine-
+    // and latency-bound and keep the default.
+    if (B > 0 && Cl >= kAllSplitMinChunk && (long long)Pmin > kNoSplitFactor * Cl) {
+      const long long c_lo = max(chunk_for(kItemsPerCtaAllSplit), (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
+      const long long c_hi = Cl + Cl * 3 / 10;
+      long long cand[kChunkCands];
+      unsigned cnt[kChunkCands];
+#pragma unroll
+      for (int k = 0; k < kChunkCands; ++k) {
+        cand[k] = c_lo + (c_hi - c_lo) * k / (kChunkCands - 1);
+        cnt[k] = 0;
+      }
+      for (int b = tid; b < B; b += nthr) {
+        const unsigned pg = (unsigned)pages_of(s_len[b]);
+#pragma unroll
+        for (int k = 0; k < kChunkCands; ++k) {
+          const unsigned c = (unsigned)cand[k];  // < 2^30 (chunks are capped at INT_MAX / 4)
+          cnt[k] += pg <= kNoSplitFactor * c ? 1u : (pg + c - 1) / c;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kChunkCands; ++k) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cnt[k] += __shfl_xor_sync(0xffffffffu, cnt[k], o);
+        if (lane == 0) s_cand[warp * kChunkCands + k] = (long long)cnt[k];
+      }
+      __syncthreads();
+      double best = 2.0;
+#pragma unroll
+      for (int k = 0; k < kChunkCands; ++k) {
+        long long n = 0;
+        for (int w = 0; w < nw; ++w) n += s_cand[w * kChunkCands + k];
+        n *= Hkv;
+        const double frac = (double)(n % num_ctas) / num_ctas;
+        const double score = fabs(frac - 0.85);
+        if (n <= items_cap && score <= best) {  // ties: the later (larger) chunk
+          best = score;
+          Cl = cand[k];
+        }
+      }
+    }
   }
   Cl = max(Cl, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
   int C = (int)min(Cl, (long long)(INT_MAX / 4));
