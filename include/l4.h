@@ -105,6 +105,9 @@ enum { L4_DECODE_EARLY_INPUTS = 1 };
  * the outputs are touched after it.  Set it only when the kernel launched immediately before on
  * the same stream cannot be writing kv_len / page_indptr.  L4_DECODE_EARLY_INPUTS implies it. */
 enum { L4_DECODE_EARLY_PLAN = 2 };
+/* Without either flag nothing is read before the previous kernel completes; the kernel only issues
+ * L2 prefetch hints (cp.async.bulk.prefetch.L2) for page_indices, q, kv_len and page_indptr as its
+ * CTAs start, which cannot return stale data (L2 is the point of coherence). */
 
 /* Bytes of device workspace needed for any batch whose page table has at most
  * max_total_pages entries (indptr[B] <= max_total_pages).  Returns 0 if the
