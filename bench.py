@@ -857,6 +857,12 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
     evs = []
     st = torch.cuda.current_stream()
     t_start = None
+    hp = {} if os.environ.get("L4_HOST_PROFILE") else None   # development: host time per loop section
+
+    def lap(key, t0):
+        if hp is not None and t_start is not None:
+            hp[key] = hp.get(key, 0.0) + time.perf_counter() - t0
+        return time.perf_counter()
     for it in range(warmup + steps):
         timed = it >= warmup
         if it == warmup:
@@ -866,13 +872,17 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
             rt.reset_stats()
             t_start = torch.cuda.Event(enable_timing=True)
             t_start.record(st)
+            host_t0 = time.perf_counter()
+        t0 = time.perf_counter()
         rt.ops.before_decode()                          # the step's decode waits for pages that landed
         kv_len, indptr = rt.device_batch()
+        t0 = lap("device_batch", t0)
         B = int(kv_len.shape[0])
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         if B > 0:
             d_len, d_ptr = rt.ops.h2d.put(kv_len, indptr)
+            t0 = lap("h2d_put", t0)
             params = l4.make_params(B, shape.num_q_heads, shape.num_kv_heads)
             qx, ox = q, out
             if e2e:
@@ -896,10 +906,13 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
                     tot["h2d"] = tot.get("h2d", 0) + B * shape.num_q_heads * 128 * 2 + 8 * B
                     tot["d2h"] = tot.get("d2h", 0) + B * shape.num_q_heads * 128 * 4
         e1.record(st)
+        t0 = lap("attention_call", t0)
         rt.ops.after_decode(e1, e0)                      # pages freed this step wait for this decode
         ev = sim.step()
+        t0 = lap("sim_step", t0)
         before = rt.stats["migrated_bytes"]
         rt.apply(ev, dist)
+        t0 = lap("apply", t0)
         if timed:
             evs.append((e0, e1, B))
             tot["kv_bytes"] += int(4 * shape.num_kv_heads * 128 * int(kv_len.sum()))
@@ -908,6 +921,7 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
             tot["steps"] += 1
             tot["mig_bytes"] += rt.stats["migrated_bytes"] - before
             tot["mig_count"] += sum(1 for m in ev.migrations if m[1] == rank)
+    host_ms = (time.perf_counter() - host_t0) * 1e3 / max(1, steps)  # enqueue time per step (host loop)
     rt.ops.drain()
     t_end = torch.cuda.Event(enable_timing=True)
     if e2e:
@@ -920,6 +934,10 @@ def run_pipeline_arm(stages, steps, warmup, rank, world, device, per_rank=256, s
         tot["lat_ms_x_req"] += dt * B
         tot["req_steps"] += B
     tot["elapsed_ms"] = t_start.elapsed_time(t_end)
+    tot["host_ms_per_step"] = host_ms
+    if hp is not None:
+        print("host ms/step by section:", {k: round(v * 1e3 / max(1, steps), 4) for k, v in hp.items()},
+              "h2d ring waits (ms, whole run):", round(rt.ops.h2d.wait_s * 1e3, 3), file=sys.stderr, flush=True)
     tot["launches"] = tot.get("launches", 0) + rt.stats["launches"]
     for k_ in ("precopy_pages", "stop_pages", "single_pages"):
         tot[k_] = rt.stats[k_]
@@ -996,7 +1014,8 @@ def pipeline_line(args, world, rank, local):
                             t["stall_ms_sum"], t["stall_count"], t["copy_ms_sum"], t["copy_bytes"],
                             t["overlap_steps"]], dtype=torch.float64, device=cdev)
         dist.all_reduce(vec, op=dist.ReduceOp.SUM)
-        tm = torch.tensor([t["elapsed_ms"], t["busy_ms"], t["stall_ms_max"]], dtype=torch.float64, device=cdev)
+        tm = torch.tensor([t["elapsed_ms"], t["busy_ms"], t["stall_ms_max"], t["host_ms_per_step"]],
+                          dtype=torch.float64, device=cdev)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         fp = torch.tensor([t["fingerprint"] & 0x7FFFFFFF], dtype=torch.int64, device=cdev)
         fps = [torch.zeros_like(fp) for _ in range(world)]
@@ -1012,7 +1031,7 @@ def pipeline_line(args, world, rank, local):
                          kv_bytes=float(vec[0]),
                          stall_ms_mean=float(vec[13]) / max(1.0, float(vec[14])), stall_ms_max=float(tm[2]),
                          copy_gbs=float(vec[16]) / max(1e-9, float(vec[15]) / 1e3) / 1e9 if vec[15] > 0 else None,
-                         copy_overlapped_steps=int(vec[17]),
+                         copy_overlapped_steps=int(vec[17]), host_ms_per_step_max=float(tm[3]),
                          stages=[list(x) for x in t["stages"]], refinements=t["refinements"])
     if rank != 0:
         return None

@@ -32,7 +32,9 @@ that sends them) have completed.
 """
 from __future__ import annotations
 
+import heapq
 import math
+import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Tuple
 
@@ -169,6 +171,7 @@ class ClusterSim:
         self.L = np.zeros(cap, dtype=np.int64)
         self.rank = np.full(cap, -1, dtype=np.int64)
         self.active = np.zeros(cap, dtype=bool)
+        self._free = list(range(cap))         # free slots, a min-heap: placement takes the lowest
         self.tokens = np.zeros(self.n_ranks, dtype=np.int64)
         self.count = np.zeros(self.n_ranks, dtype=np.int64)
         self.queue: List[Tuple[int, int, int]] = []
@@ -187,8 +190,8 @@ class ClusterSim:
     # ---------------------------------------------------------------- routing
     def stage_of(self, L: int) -> int:
         """Earliest stage whose range covers length L; the last stage takes the rest."""
-        for k in range(self.last_stage):
-            if L < self.bounds[k]:
+        for k, b in enumerate(self.bounds.tolist()[: self.last_stage]):
+            if L < b:
                 return k
         return self.last_stage
 
@@ -233,19 +236,27 @@ class ClusterSim:
         return best
 
     def _free_slot(self):
-        free = np.nonzero(~self.active)[0]
-        if free.size == 0:
+        """The lowest free slot (a min-heap of free slots; the arrays double when none is left)."""
+        if not self._free:
             n = self.rid.size
             for name in ("rid", "I", "O", "L", "rank"):
                 arr = getattr(self, name)
                 fill = -1 if name in ("rid", "rank") else 0
                 setattr(self, name, np.concatenate([arr, np.full(n, fill, dtype=arr.dtype)]))
             self.active = np.concatenate([self.active, np.zeros(n, dtype=bool)])
-            return n
-        return int(free[0])
+            self._free = list(range(n, 2 * n))
+        return heapq.heappop(self._free)
 
-    def _place(self, rid, I, O, L, initial=False):
-        r = self.least_loaded(self.stage_of(L), L + 1)
+    def _place(self, rid, I, O, L, initial=False, fail_cache=None):
+        k = self.stage_of(L)
+        # within one arrivals pass capacity only shrinks, so once no instance of stage k fits
+        # `extra` tokens, none fits more (exact shortcut for the queued retries)
+        if fail_cache is not None and L + 1 >= fail_cache.get(k, 1 << 62):
+            r = None
+        else:
+            r = self.least_loaded(k, L + 1)
+            if r is None and fail_cache is not None:
+                fail_cache[k] = min(fail_cache.get(k, 1 << 62), L + 1)
         if r is None:
             if not initial:
                 self.queue.append((rid, I, O))
@@ -273,6 +284,7 @@ class ClusterSim:
             self.tokens[r] -= self.L[i]
             self.count[r] -= 1
             self.active[i] = False
+            heapq.heappush(self._free, int(i))
         # 2b. live sessions of retired requests are dropped (the receiver frees its copy)
         for rid, r in ev.retired:
             ses = self.sessions.pop(rid, None)
@@ -330,8 +342,9 @@ class ClusterSim:
         pending, self.queue = self.queue, []
         for _ in range(len(done)):
             pending.append(self.stream.next())
+        fail_cache = {}
         for rid, I, O in pending:
-            r = self._place(rid, I, O, I)
+            r = self._place(rid, I, O, I, fail_cache=fail_cache)
             if r is not None:
                 ev.admitted.append((rid, r, I))
         return ev
@@ -544,13 +557,22 @@ class RankRuntime:
         # growth: the step's new token opens a new page when L-1 is a multiple of 16
         sim = self.sim
         mig_out = {m[0] for m in ev.migrations if m[1] == me} | {p[0] for p in ev.precopies if p[1] == me}
-        grow = np.nonzero(sim.active & ((sim.L - 1) % PAGE == 0))[0]
-        for i in grow:
-            rid = int(sim.rid[i])
-            if rid in self.pages and (int(sim.rank[i]) == me or rid in mig_out):
-                need = -(-int(sim.L[i]) // PAGE)
-                if need > len(self.pages[rid]):
-                    self._append(rid, self.ops.alloc(self.pool, need - len(self.pages[rid])))
+        mine = sim.rank == me
+        if mig_out:
+            mine = mine | np.isin(sim.rid, np.fromiter(mig_out, dtype=np.int64, count=len(mig_out)))
+        grow = np.nonzero(sim.active & mine & ((sim.L - 1) % PAGE == 0))[0]
+        wants = []
+        for rid, L in zip(sim.rid[grow].tolist(), sim.L[grow].tolist()):
+            if rid in self.pages:
+                n = -(-L // PAGE) - len(self.pages[rid])
+                if n > 0:
+                    wants.append((rid, n))
+        if wants:  # one lowest-free-first allocation for all of them, dealt out in the same order
+            got = self.ops.alloc(self.pool, sum(n for _, n in wants))
+            o = 0
+            for rid, n in wants:
+                self._append(rid, got[o:o + n])
+                o += n
         for rid, dst in ev.cancelled:                 # live session of a retired request
             if dst == me and rid in self.incoming:
                 self.ops.free(self.pool, self.incoming.pop(rid))
@@ -604,13 +626,14 @@ class H2DRing:
     one slot and moved with one async copy on the current stream.  A slot is reused only after
     its previous copy completed (event).  Arrays larger than a slot take the plain path."""
 
-    def __init__(self, device, slot_bytes: int = 1 << 20, depth: int = 4):
+    def __init__(self, device, slot_bytes: int = 1 << 20, depth: int = 16):
         import torch
         self.torch, self.device, self.slot_bytes, self.depth = torch, device, slot_bytes, depth
         self.h = [torch.empty(slot_bytes, dtype=torch.uint8).pin_memory() for _ in range(depth)]
         self.d = [torch.empty(slot_bytes, dtype=torch.uint8, device=device) for _ in range(depth)]
         self.ev = [None] * depth
         self.i = 0
+        self.wait_s = 0.0   # host time spent waiting for a slot's previous copy (device behind)
 
     def put(self, *arrays):
         torch = self.torch
@@ -624,7 +647,9 @@ class H2DRing:
         k = self.i % self.depth
         self.i += 1
         if self.ev[k] is not None:
+            t0 = time.perf_counter()
             self.ev[k].synchronize()
+            self.wait_s += time.perf_counter() - t0
         hv = self.h[k].numpy()
         for a, o in zip(arrays, offs):
             hv[o:o + a.nbytes] = a.view(np.uint8)
