@@ -156,6 +156,7 @@ class ClusterSim:
         self.refine_alpha, self.min_traffic = float(refine_alpha), int(min_traffic)
         self.rank_hi = self.stage_hi[self.rank_stage].astype(np.float64)
         self.bounds = self.stage_hi.astype(np.float64)           # routing upper bound per stage
+        self._bounds_l = self.bounds.tolist()[: len(self.stages) - 1]   # (Python copy for stage_of)
         self.refinements = 0
         self.last_stage = len(self.stages) - 1
         self.stage_ranks = [[r for r in range(self.n_ranks) if self.rank_stage[r] == k] for k in range(len(self.stages))]
@@ -190,7 +191,7 @@ class ClusterSim:
     # ---------------------------------------------------------------- routing
     def stage_of(self, L: int) -> int:
         """Earliest stage whose range covers length L; the last stage takes the rest."""
-        for k, b in enumerate(self.bounds.tolist()[: self.last_stage]):
+        for k, b in enumerate(self._bounds_l):
             if L < b:
                 return k
         return self.last_stage
@@ -381,6 +382,7 @@ class ClusterSim:
         self.rank_hi = new_hi
         for k in range(self.last_stage):
             self.bounds[k] = float(np.mean([self.rank_hi[r] for r in self.stage_ranks[k]]))
+        self._bounds_l = self.bounds.tolist()[: self.last_stage]
         self.refinements += 1
 
     def _move(self, i, src, dst, L):
