@@ -105,6 +105,7 @@ constexpr int kQuadTailPerCta = L4_QUAD_TAIL;  // CTA-wide items per CTA at the 
 #define L4_QUAD_MIN 4
 #endif
 constexpr int kQuadMinPerCta = L4_QUAD_MIN;  // quads only if there are at least this many per CTA
+constexpr int kQuadPagesPerUnitCta = 10;       // ... or q_pages / 10 if fewer (>= 1 per CTA)
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kLog2e = 1.44269504088896340736f;
 
@@ -1205,9 +1206,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   // warp alone streams a page at a fraction of a CTA's share of HBM bandwidth).
   const int q_rest = n_items - n_wide;
   int n_quads = (q_rest - min(q_rest, kQuadTailPerCta * W)) / kQuad;
-  // A quad is the launch's granularity at the end: units of at most ~16 pages need one per CTA,
-  // larger ones up to kQuadMinPerCta per CTA (q_pages = pages of the largest quad item)
-  if (n_quads < min(kQuadMinPerCta, max(1, (q_pages + 3) / 4)) * W) n_quads = 0;
+  // A quad is the launch's granularity at the end, so quads need q_pages / kQuadPagesPerUnitCta
+  // units per CTA, at least 1 and at most kQuadMinPerCta (q_pages = pages of the largest quad
+  // item).  Measured (plain calls, units per CTA -> quads vs CTA-wide items): 13-page items at
+  // 1.7 / 2.0 / 3.5 per CTA 37.7 vs 42.2 / 49.9 vs 51.7 / 72.3 vs 80.0 us (70B shape: 38.9 vs
+  // 51.0 at 1.7 per CTA); 25-page items at 1.35 per CTA 63.0 vs 57.3 (worse), at 2.7 99.7 vs
+  // 103.8; 50-page items at 1.1 per CTA 114 vs 86 (worse).  (Round 1's rule, min(4, pages / 4)
+  // per CTA, predates the quad pacing and epilogue of late round 2.)
+  if (kQuadPagesPerUnitCta * n_quads < min(kQuadMinPerCta * kQuadPagesPerUnitCta, max(kQuadPagesPerUnitCta, q_pages)) * W)
+    n_quads = 0;
   const int n_units = n_items - (kQuad - 1) * n_quads;
   const int u_tail = n_wide + n_quads;  // first tail unit
   if (threadIdx.x == 0) L4_MARK(2);
