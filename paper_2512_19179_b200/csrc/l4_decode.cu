@@ -79,6 +79,9 @@ constexpr int kItemsPerCta = L4_ITEMS_PER_CTA;        // automatic chunk target
 constexpr int kItemsPerCtaAllSplit = L4_ITEMS_PER_CTA_ALL_SPLIT;  // ... when every request is split
 constexpr int kAllSplitMinChunk = 128;  // ... and the default chunk has at least this many pages
 constexpr int kChunkCands = 16;         // chunk candidates of a large all-split batch
+#ifndef L4_CHUNK_SEARCH
+#define L4_CHUNK_SEARCH 1
+#endif
 constexpr int kNoSplitFactor = 2;                     // requests of <= 2C pages are never split
 constexpr int kMaxBatch = 8192;
 constexpr int kPlanThreads = 1024;
@@ -304,9 +307,62 @@ __device__ __forceinline__ int bin_of(int pages, int nsplit) {
   return min(kNumBins - 1, 32 - __clz(ip));      // bit_length(ip)
 }
 
+// Chunk choice of a large all-split batch (plan_core, §4.1): among kChunkCands chunks from c12 (12
+// items per CTA) to 1.3x the default chunk c8, the one whose last round of items is closest to 85%
+// full (ties: the larger chunk).  Block-wide (every thread calls it); s_cand aliases s_wcnt, which
+// it leaves zeroed.  Kept out of line: inlined, its unrolled code cost mixed batches 0.3-0.5%
+// (measured with it compiled out), although they never execute it.
+__device__ __noinline__ long long chunk_search(const int* s_len, int B, int Hkv, int num_ctas, int items_cap,
+                                               int Pmax, long long c8, long long c12, long long* s_cand,
+                                               int* s_wcnt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x, nw = nthr >> 5;
+  long long Cl = c8;
+  const long long c_lo = max(c12, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
+  const long long c_hi = c8 + c8 * 3 / 10;
+  long long cand[kChunkCands];
+  unsigned cnt[kChunkCands];
+#pragma unroll
+  for (int k = 0; k < kChunkCands; ++k) {
+    cand[k] = c_lo + (c_hi - c_lo) * k / (kChunkCands - 1);
+    cnt[k] = 0;
+  }
+  for (int b = tid; b < B; b += nthr) {
+    const unsigned pg = (unsigned)pages_of(s_len[b]);
+#pragma unroll
+    for (int k = 0; k < kChunkCands; ++k) {
+      const unsigned c = (unsigned)cand[k];  // < 2^30 (chunks are capped at INT_MAX / 4)
+      cnt[k] += pg <= kNoSplitFactor * c ? 1u : (pg + c - 1) / c;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kChunkCands; ++k) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt[k] += __shfl_xor_sync(0xffffffffu, cnt[k], o);
+    if (lane == 0) s_cand[warp * kChunkCands + k] = (long long)cnt[k];
+  }
+  __syncthreads();
+  double best = 2.0;
+#pragma unroll
+  for (int k = 0; k < kChunkCands; ++k) {
+    long long n = 0;
+    for (int w = 0; w < nw; ++w) n += s_cand[w * kChunkCands + k];
+    n *= Hkv;
+    const double frac = (double)(n % num_ctas) / num_ctas;
+    const double score = fabs(frac - 0.85);
+    if (n <= items_cap && score <= best) {  // ties: the later (larger) chunk
+      best = score;
+      Cl = cand[k];
+    }
+  }
+  __syncthreads();  // every thread read s_cand: give s_wcnt back to pass 1, zeroed
+  for (int x = tid; x < nw * kNumBins; x += nthr) s_wcnt[x] = 0;
+  __syncthreads();
+  return Cl;
+}
+
 // Shared-memory scratch of plan_core (bytes; 8-byte aligned base).
-constexpr int kPlanScratchBytes =
-    32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * 16 * 8;
+constexpr int kPlanScratchBytes = 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4 + kPlanMaxWarps * kNumBins * 4 + 32 * 4 + 32 * 4;
 
 // The planner (a1), run by every thread of a CTA: reads kv_len / indptr, chooses the chunk C,
 // and orders the requests by length bin, longest bin first, request index ascending inside a
@@ -328,7 +384,10 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   int* s_wcnt = reinterpret_cast<int*>(scratch + 32 * 8 + 36 * 4 + 32 * 4 + 32 * 4);  // [nw][kNumBins]
   int* s_ms = s_wcnt + kPlanMaxWarps * kNumBins;  // per-warp lowest bin of a split request
   int* s_mn = s_ms + 32;                           // per-warp smallest page count
-  long long* s_cand = reinterpret_cast<long long*>(s_mn + 32);  // [nw][kChunkCands] item counts
+  // [nw][kChunkCands] item counts of the chunk search: aliases the per-warp bin counts s_wcnt
+  // (same size), which are re-zeroed after the search
+  long long* s_cand = reinterpret_cast<long long*>(s_wcnt);
+  static_assert(kChunkCands * 8 == kNumBins * 4, "s_cand aliases s_wcnt");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nw = nthr >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -417,45 +476,8 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     // C4 1588 -> 1571 us, 25 x 39454 591 -> 586, 64 x 16384 623 -> 619, 12 x 84547 and 8 x 131072
     // unchanged.  Small all-split batches (default chunk < kAllSplitMinChunk pages) are combine-
     // and latency-bound and keep the default.
-    if (B > 0 && Cl >= kAllSplitMinChunk && (long long)Pmin > kNoSplitFactor * Cl) {
-      const long long c_lo = max(chunk_for(kItemsPerCtaAllSplit), (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
-      const long long c_hi = Cl + Cl * 3 / 10;
-      long long cand[kChunkCands];
-      unsigned cnt[kChunkCands];
-#pragma unroll
-      for (int k = 0; k < kChunkCands; ++k) {
-        cand[k] = c_lo + (c_hi - c_lo) * k / (kChunkCands - 1);
-        cnt[k] = 0;
-      }
-      for (int b = tid; b < B; b += nthr) {
-        const unsigned pg = (unsigned)pages_of(s_len[b]);
-#pragma unroll
-        for (int k = 0; k < kChunkCands; ++k) {
-          const unsigned c = (unsigned)cand[k];  // < 2^30 (chunks are capped at INT_MAX / 4)
-          cnt[k] += pg <= kNoSplitFactor * c ? 1u : (pg + c - 1) / c;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kChunkCands; ++k) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) cnt[k] += __shfl_xor_sync(0xffffffffu, cnt[k], o);
-        if (lane == 0) s_cand[warp * kChunkCands + k] = (long long)cnt[k];
-      }
-      __syncthreads();
-      double best = 2.0;
-#pragma unroll
-      for (int k = 0; k < kChunkCands; ++k) {
-        long long n = 0;
-        for (int w = 0; w < nw; ++w) n += s_cand[w * kChunkCands + k];
-        n *= Hkv;
-        const double frac = (double)(n % num_ctas) / num_ctas;
-        const double score = fabs(frac - 0.85);
-        if (n <= items_cap && score <= best) {  // ties: the later (larger) chunk
-          best = score;
-          Cl = cand[k];
-        }
-      }
-    }
+    if (L4_CHUNK_SEARCH && B > 0 && Cl >= kAllSplitMinChunk && (long long)Pmin > kNoSplitFactor * Cl)
+      Cl = chunk_search(s_len, B, Hkv, num_ctas, items_cap, Pmax, Cl, chunk_for(kItemsPerCtaAllSplit), s_cand, s_wcnt);
   }
   Cl = max(Cl, (long long)((Pmax + kMaxSplits - 1) / kMaxSplits));
   int C = (int)min(Cl, (long long)(INT_MAX / 4));
