@@ -257,7 +257,6 @@ struct PlanArgs {
 };
 
 constexpr int kPlanMaxWarps = kPlanThreads / 32;
-constexpr int kPlanUnroll = 8;  // request tiles per warp whose shared loads the planner issues together
 
 // Block-wide (sum int64, max int, min int, or bits) in one pass.
 __device__ void block_reduce4(long long v, int m, int mn, unsigned bits, long long* s_ll, int* s_i, int* s_mn,
@@ -509,34 +508,23 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   int min_split_bin;
   for (;;) {
     int wsum = 0, wms = kNumBins;
-    // pass 1: per-warp bin histogram + item count, 8 tiles at a time with their loads issued
-    // together (a tile-by-tile loop serialised each shared load behind the previous tile's
-    // stores and atomics: ~0.2 us per tile at B = 1024)
-    for (int t0 = r0; t0 < r1; t0 += kPlanUnroll * 32) {
-      int Lr[kPlanUnroll];
-#pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i) {
-        const int b = t0 + i * 32 + lane;
-        Lr[i] = b < r1 ? s_len[b] : 0;
+    // pass 1: per-warp bin histogram + item count, tile by tile (a version that issued the shared
+    // loads of 8 tiles together measured the same: random-composition sweep, scripts/gpu_run35.sh)
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+      const int b = t0 + lane;
+      int bin = -1;
+      if (b < r1) {
+        const int pg = pages_of(s_len[b]);
+        const int ns = nsplit_of(pg, C);
+        bin = bin_of(pg, ns);
+        wsum += ns;
+        if (ns > 1) wms = min(wms, bin);
+        s_off[b] = bin | (ns << 16);  // kept for pass 2 (s_off is free until the scan)
       }
-#pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i) {
-        if (t0 + i * 32 >= r1) break;  // warp-uniform
-        const int b = t0 + i * 32 + lane;
-        int bin = -1;
-        if (b < r1) {
-          const int pg = pages_of(Lr[i]);
-          const int ns = nsplit_of(pg, C);
-          bin = bin_of(pg, ns);
-          wsum += ns;
-          if (ns > 1) wms = min(wms, bin);
-          s_off[b] = bin | (ns << 16);  // kept for pass 2 (s_off is free until the scan)
-        }
-        // one shared atomic per distinct bin of the tile (counts only: tiles independent); a
-        // lane-per-lane atomic serialises 32 ways on a homogeneous batch
-        const unsigned peers = __match_any_sync(0xffffffffu, bin);
-        if (bin >= 0 && (peers & lt_mask) == 0) atomicAdd(&s_wcnt[warp * kNumBins + bin], __popc(peers));
-      }
+      // one shared atomic per distinct bin of the tile (counts only: tiles independent; per-lane
+      // atomics serialise on a tile of equal bins: B = 128 short requests 45.0 -> 43.4 us)
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (bin >= 0 && (peers & lt_mask) == 0) atomicAdd(&s_wcnt[warp * kNumBins + bin], __popc(peers));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -592,40 +580,26 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
   const bool one_bin = s_i[33] != 0;
   if (tid == 0) L4_MARK(8);
   if (one_bin) {  // fast path, same result: a stable sort of one bin is the identity
-    for (int b0 = tid; b0 < B; b0 += kPlanUnroll * nthr) {
-      int pk[kPlanUnroll];
-#pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i) pk[i] = b0 + i * nthr < B ? s_off[b0 + i * nthr] : 0;
-#pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i)
-        if (b0 + i * nthr < B) s_rb[b0 + i * nthr] = (b0 + i * nthr) | ((pk[i] >> 16) << 16);
-    }
+    for (int b = tid; b < B; b += nthr) s_rb[b] = b | ((s_off[b] >> 16) << 16);
   } else {
-    for (int t0 = r0; t0 < r1; t0 += kPlanUnroll * 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
-      int pk[kPlanUnroll];
-#pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i) pk[i] = t0 + i * 32 + lane < r1 ? s_off[t0 + i * 32 + lane] : 0;
-#pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i) {
-        if (t0 + i * 32 >= r1) break;  // warp-uniform
-        const int b = t0 + i * 32 + lane;
-        int bin = -1, ns = 0;
-        if (b < r1) {
-          const int packed = pk[i];                   // pass 1's (bin, nsplit)
-          bin = packed & 0xffff;
-          ns = packed >> 16;
-        }
-        const unsigned peers = __match_any_sync(0xffffffffu, bin);
-        const int lower = __popc(peers & lt_mask);
-        int pos = 0;
-        if (bin >= 0) pos = s_wcnt[warp * kNumBins + bin] + lower;
-        __syncwarp();
-        if (bin >= 0) {
-          s_rb[pos] = b | (ns << 16);  // b < 8192, ns <= kMaxSplits
-          if (lower == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
-        }
-        __syncwarp();
+    for (int t0 = r0; t0 < r1; t0 += 32) {  // pass 2: scatter (request | nsplit << 16) to its rank
+      const int b = t0 + lane;
+      int bin = -1, ns = 0;
+      if (b < r1) {
+        const int packed = s_off[b];                // pass 1's (bin, nsplit)
+        bin = packed & 0xffff;
+        ns = packed >> 16;
       }
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      const int lower = __popc(peers & lt_mask);
+      int pos = 0;
+      if (bin >= 0) pos = s_wcnt[warp * kNumBins + bin] + lower;
+      __syncwarp();
+      if (bin >= 0) {
+        s_rb[pos] = b | (ns << 16);  // b < 8192, ns <= kMaxSplits
+        if (lower == 0) s_wcnt[warp * kNumBins + bin] += __popc(peers);
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -647,23 +621,17 @@ __device__ void plan_core(const int* __restrict__ kv_len, const int* __restrict_
     int carry = 0;
     for (int w = 0; w < warp; ++w) carry += s_w[w];
     carry *= Hkv;
-    for (int t0 = r0; t0 < r1; t0 += kPlanUnroll * 32) {
-      int cr[kPlanUnroll];
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+      const int r = t0 + lane;
+      const int cnt = r < r1 ? (s_rb[r] >> 16) * Hkv : 0;
+      int incl = cnt;
 #pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i) cr[i] = t0 + i * 32 + lane < r1 ? (s_rb[t0 + i * 32 + lane] >> 16) * Hkv : 0;
-#pragma unroll
-      for (int i = 0; i < kPlanUnroll; ++i) {
-        if (t0 + i * 32 >= r1) break;  // warp-uniform
-        const int r = t0 + i * 32 + lane;
-        int incl = cr[i];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        if (r < r1) s_off[r] = carry + incl - cr[i];
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
+      if (r < r1) s_off[r] = carry + incl - cnt;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (tid == 0) s_off[B] = (int)N;
   }
