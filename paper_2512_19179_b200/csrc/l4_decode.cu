@@ -14,7 +14,9 @@
 //      inefficiency).  Run by EVERY CTA of the single-launch path
 //      (l4_decode_attention: the plan stays in shared memory, no planner launch)
 //      or by plan_kernel (l4_decode_plan: a materialised work list reused by
-//      l4_decode_run, e.g. for every layer of a step).
+//      l4_decode_run, e.g. for every layer of a step).  Unsplit single-bin
+//      batches skip the sort; large all-split batches pick the chunk whose last
+//      round of items is ~85% full (chunk_search).
 //  a2  decode_kernel (persistent, 1 producer + 4 consumer warps per CTA,
 //      2 CTAs per SM): items are handed out dynamically (first one static,
 //      then one atomic ticket per unit), so CTAs that finish early
@@ -25,13 +27,17 @@
 //      S^T = K Q^T and O^T += V^T P^T with mma.sync m16n8k16 (tokens / head_dim
 //      on M, the G <= 8 query heads on N, so GQA group 8 has no padding), an
 //      online softmax with warp-shuffle max reductions in the exp2 domain, and
-//      P split into bf16 hi + lo (Z23).  With L4_DECODE_EARLY_INPUTS the next
-//      call plans and streams its first item while this one finishes (PDL).
-//      Quad units: when the short unsplit items at the end of the LPT order
-//      are numerous (>= 4 units of four per CTA), they are handed
-//      out four at a time, one whole item per consumer warp (pages of the four
-//      items interleaved in the ring), with no cross-warp merge or CTA barrier
-//      per item: short-request batches stop paying a merge per few pages.
+//      P split into bf16 hi + lo (Z23); a stage goes back to the producer as
+//      soon as its K and V fragments are in registers.  With
+//      L4_DECODE_EARLY_INPUTS the next call plans and streams its first item
+//      while this one finishes (PDL); every call issues L2 prefetch hints for
+//      its first inputs at entry.  Quad units: when the short unsplit items at
+//      the end of the LPT order are numerous enough (clamp(pages / 10, 1, 4)
+//      units of four per CTA), they are handed out four at a time, one whole
+//      item per consumer warp (pages of the four items interleaved in the ring;
+//      the next unit's ticket and page ids fetched while this one's pages go
+//      out), with no cross-warp merge or CTA barrier per item: short-request
+//      batches stop paying a merge per few pages.
 //  a3  LSE combine: the 4 warps of a CTA merge their (m, l, O) in shared
 //      memory; a split item writes (O/l, lse) to the workspace; the last split
 //      of each group of 16 combines the group, the last group combines the
