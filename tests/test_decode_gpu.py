@@ -404,6 +404,29 @@ def test_quad_units_short_batch(G, chunk):
     assert torch.equal(lb, l2)
 
 
+@pytest.mark.parametrize("G", [4, 8])
+def test_quad_units_few_per_cta(G):
+    """The late round-2 quad admission rule (clamp(pages / 10, 1, 4) units per CTA): B = 256
+    requests of ~200 tokens give 512 quad units, ~1.7 per CTA, so most CTAs run one or two quads
+    and the launch ends on them.  Ragged lengths with NaN-poisoned tails, fused == plan + run
+    bitwise, repeated calls bitwise, oracle within 2e-3."""
+    rng = np.random.default_rng(500 + G)
+    lens = rng.integers(150, 209, size=256)
+    lens[:3] = [0, 1, 208]
+    Hkv = 8
+    table, ro, rl, qd, kd, vd, ip, ix, kl = _dev_case(lens, Hkv * G, Hkv, seed=G)
+    params = l4.make_params(table.batch, Hkv * G, Hkv)
+    ws = l4.alloc_workspace(params, table.total_pages)
+    o1, l1 = _plan_run(params, table, qd, kd, vd, ip, ix, kl, ws)
+    o2, l2 = _fused(params, table, qd, kd, vd, ip, ix, kl, ws)
+    again = [_fused(params, table, qd, kd, vd, ip, ix, kl, ws) for _ in range(3)]
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    for o3, l3 in again:
+        assert torch.equal(o2, o3) and torch.equal(l2, l3)
+    _check(o2.double().cpu().numpy(), l2.double().cpu().numpy(), ro, rl)
+
+
 @pytest.mark.parametrize("Hq", [32, 64])
 def test_quad_units_materialised_plan(Hq):
     """B > 1024 takes the materialised plan (planner kernel + run kernel): quad units there too,
