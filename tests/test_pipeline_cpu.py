@@ -25,6 +25,40 @@ def test_assign_and_route():
         assert sim.rank_stage[q.rank] == sim.stage_of(q.L)
 
 
+def test_sim_placements_take_the_lowest_free_slot_and_skip_only_unplaceable_arrivals():
+    """The control plane's fast paths change no decision: every placement takes the lowest inactive
+    slot (the free-slot min-heap vs a scan of the active mask), and an arrival the pass skips
+    through its capacity shortcut is one that no instance of its stage could take."""
+    stages, _ = pipeline.plan_stages(4, seed=0, n_sample=2000)
+    sim = pipeline.ClusterSim(stages, concurrency=4 * 256, seed=5, token_budget=300_000, policy="bidask",
+                              rebalance_every=10, precopy_lead=8)
+    orig_free, orig_ll = sim._free_slot, sim.least_loaded
+    checked = {"slots": 0, "skips": 0}
+
+    def free_slot():
+        inactive = np.nonzero(~sim.active)[0]
+        i = orig_free()
+        if inactive.size:
+            assert i == int(inactive[0])
+            checked["slots"] += 1
+        return i
+
+    sim._free_slot = free_slot
+    orig_place = sim._place
+
+    def place(rid, I, O, L, initial=False, fail_cache=None):
+        k = sim.stage_of(L)
+        if fail_cache is not None and L + 1 >= fail_cache.get(k, 1 << 62):
+            assert orig_ll(k, L + 1) is None     # the shortcut only skips what would fail anyway
+            checked["skips"] += 1
+        return orig_place(rid, I, O, L, initial=initial, fail_cache=fail_cache)
+
+    sim._place = place
+    for _ in range(300):
+        sim.step()
+    assert checked["slots"] > 100 and checked["skips"] > 0, checked
+
+
 def test_sim_deterministic_and_conserving():
     stages, _ = pipeline.plan_stages(4, seed=0, n_sample=2000)
     a = pipeline.ClusterSim(stages, concurrency=256, seed=3)
